@@ -1,0 +1,353 @@
+"""Benchmark of the LongLive-2.0 NVFP4 KV-cache hot path on B200 (driver contract: one JSON line).
+
+Metric (BASELINE.json): attention query-tokens/s and KV HBM GB/s (% roofline).  Workload at N=1
+is BASELINE.json configs[1], the Wan2.1-1.3B-shaped single layer: 12 heads x 128, chunk =
+3 latent frames x 1560 tokens (T_c = 4680), window 21 frames incl. the current chunk + 3-frame
+sink -> |K_eff| = 32,760 keys (chunk 6 of a rollout: 7 resident chunks).  One STEP = the whole
+hot path for one (layer, chunk): kv_quantize_append(K, V) of the new chunk + chunk_attention of
+its queries over the quantized window with fused dequant.  value = T_c / step time.
+
+N>1 (torchrun, one process per GPU): the same layer step head-sharded Ulysses-style
+(PAPER.md:556-564): pack -> NCCL all-to-all -> append + attention on the local heads -> NCCL
+all-to-all of O -> unpack.  value = T_c / max-over-ranks step time (strong scaling: the layer
+shape is fixed).
+
+--impl reference: the float64 CPU oracle (oracle/) on the host cores, each step a bounded
+sample of the same workload, printed with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_FRAMES, TPF, H, D = 3, 1560, 12, 128
+T_C = T_FRAMES * TPF
+SINK, WINDOW = 3, 21
+CHUNK = 6                      # chunk index whose step is timed: 7 resident chunks, 32,760 keys
+METRIC = "attention query-tokens/s and KV HBM GB/s (% roofline) at 1/2/4/8 B200"
+WORKLOAD = "Wan2.1-1.3B-shaped single layer (BASELINE.json configs[1])"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            P = json.load(f)
+        return P["hbm_gbs"], P["bf16_tflops"], P.get("bf16_tflops_sustained", P["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def n_keys():
+    # |K_eff(6)| with a 3-frame sink and 21-frame window: frames [0, 21) -> 32,760 tokens
+    f_end = (CHUNK + 1) * T_FRAMES
+    frames = set(range(0, min(SINK, f_end))) | set(range(max(0, f_end - WINDOW), f_end))
+    return len(frames) * TPF
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample(q_rows=16, quant_frac=8):
+    """Time the oracle (as it stands) on a bounded sample of one step; returns (est step s, desc)."""
+    from oracle import nvfp4
+    from oracle.attention import attention
+    from oracle.keyset import key_token_ranges
+    from paper_2605_18739_b200 import synth
+
+    q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, CHUNK)
+    rows = T_C // quant_frac
+    t0 = time.perf_counter()
+    nvfp4.quantize_kv_chunk(k.f64[:rows])
+    nvfp4.quantize_kv_chunk(v.f64[:rows])
+    t_quant = (time.perf_counter() - t0) * quant_frac
+    # dequantize the window (7 chunks of K and V) -- one chunk timed, x7
+    qk = nvfp4.quantize_kv_chunk(k.f64)
+    t0 = time.perf_counter()
+    Kc = nvfp4.dequantize_kv_chunk(qk, T_C, H, D)
+    t_deq = (time.perf_counter() - t0) * 2 * (n_keys() // T_C)
+    nk = n_keys()
+    Kw = np.concatenate([Kc] * (nk // T_C))
+    rows_idx = np.linspace(0, T_C - 1, q_rows).astype(int)
+    t0 = time.perf_counter()
+    attention(q.f64, Kw, Kw, rows=rows_idx)
+    t_att = (time.perf_counter() - t0) * T_C / q_rows
+    est = t_quant + t_deq + t_att
+    desc = (f"quantize {rows} of {T_C} tokens (x{quant_frac}) + dequantize 1 of {2 * nk // T_C} window chunk "
+            f"tensors (x{2 * nk // T_C}) + attention for {q_rows} of {T_C} query rows over {nk} keys "
+            f"(x{T_C // q_rows}); extrapolated to one full step")
+    return est, desc
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_18739_b200 import kvq, synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    P = world
+    h0, h1 = kvq.head_partition(H, P, rank)
+    Hr = h1 - h0
+    nk = n_keys()
+
+    cache = kvq.KVCache(1, Hr, D, TPF, T_FRAMES, sink_frames=SINK, window_frames=WINDOW, max_chunk_slots=8,
+                        device=dev)
+    mask = kvq.Mask(CHUNK, SINK, WINDOW)
+    Ts = T_C // P
+    # synthetic chunk data (seeded); each rank holds its sequence shard of the full [T_c, H, d]
+    chunks = []
+    for ch in range(CHUNK + 1):
+        q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, ch)
+        chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
+    dq = [tuple(x.to(dev) for x in c) for c in chunks]
+    uly = kvq.Ulysses(cache, H, D, T_C, rank, P) if P > 1 else None
+
+    def step(c, out=None):
+        q, k, v = dq[c]
+        if uly is None:
+            cache.append(0, c, k, v)
+            return cache.attention(0, q, mask if c == CHUNK else kvq.Mask(c, SINK, WINDOW), out=out)
+        return uly.step(0, c, q, k, v, mask if c == CHUNK else kvq.Mask(c, SINK, WINDOW), out=out)
+
+    for c in range(CHUNK):          # fill the window: chunks 0..5
+        step(c)
+    # the timed step re-writes chunk 6 each time (a denoising step of the in-progress chunk)
+    O = torch.empty((Ts, H, D), dtype=torch.bfloat16, device=dev)
+    step(CHUNK, O)
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev_att = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev_app = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    q6, k6, v6 = dq[CHUNK]
+    Olocal = torch.empty((T_C, Hr, D), dtype=torch.bfloat16, device=dev)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(CHUNK, O)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                                  # L2 flushed before every step
+            ev[i][0].record(st)
+            step(CHUNK, O)
+            ev[i][1].record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        # per-kernel timing on this rank's local head set (1-GPU shapes when P = 1)
+        if uly is None:
+            for i in range(args.steps):
+                flush.zero_()
+                ev_app[i][0].record(st)
+                cache.append(0, CHUNK, k6, v6)
+                ev_app[i][1].record(st)
+                flush.zero_()
+                ev_att[i][0].record(st)
+                cache.attention(0, q6, mask, out=O)
+                ev_att[i][1].record(st)
+            torch.cuda.synchronize()
+    step_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    value = T_C / (step_ms * 1e-3)
+
+    # ---- end-to-end through the public API with host buffers (pinned), copies inside the region
+    e2e = None
+    if uly is None:
+        hq, hk, hv = (x.pin_memory() for x in chunks[CHUNK])
+        hO = torch.empty((T_C, H, D), dtype=torch.bfloat16).pin_memory()
+        gq, gk, gv = (torch.empty_like(x, device=dev) for x in (hq, hk, hv))
+        for _ in range(2):
+            gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
+            cache.append(0, CHUNK, gk, gv)
+            cache.attention(0, gq, mask, out=O)
+            hO.copy_(O, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
+            cache.append(0, CHUNK, gk, gv)
+            cache.attention(0, gq, mask, out=O)
+            hO.copy_(O, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
+        e2e = {"value": T_C / (e2e_ms * 1e-3), "unit": "query-tokens/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hO.numel() * 2)}
+
+    hbm, tf_burst, tf_sus, src = peaks()
+    flops = 4.0 * T_C * nk * D * H
+    out = {"metric": METRIC, "value": value, "unit": "query-tokens/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "nvfp4 KV (e2m1/e4m3/fp32 "
+           "scales), fp16 tensor-core MMA with fp32 accumulate, bf16 Q/K/V/O",
+           "data": "synthetic (seeded SplitMix64 -> Box-Muller N(0,1) -> bf16; no weights needed)",
+           "config": {"workload": WORKLOAD, "heads": H, "head_dim": D, "T_c": T_C, "tokens_per_frame": TPF,
+                      "frames_per_chunk": T_FRAMES, "sink_frames": SINK, "window_frames": WINDOW,
+                      "n_keys": nk, "chunk_index": CHUNK, "parallelism": f"ulysses-heads{world}" if world > 1 else "1 GPU",
+                      "l2": "flushed (256 MiB write) before every timed step"},
+           "gpu_launches": args.steps * (3 if world == 1 else 6)}
+    if uly is None:
+        att_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_att]))
+        app_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
+        ach = flops / (att_ms * 1e-3) / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get("attn_kernel")
+        except Exception:
+            pass
+        out["roofline"] = {"bound": "tensor", "kernel": "attn_kernel (fused dequant + QK^T + softmax + PV)",
+                           "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus,
+                           "traffic": traffic, "peak_source": f"{src} bf16_tflops_sustained (fp16 kind::f16 = same rate)",
+                           "frac_of_burst": ach / tf_burst, "ms": att_ms, "flops_per_launch": flops}
+        app_bytes = T_C * H * D * 2 * (2 + 9 / 16)
+        out["roofline_append"] = {"bound": "hbm", "kernel": "amax_kernel + quant_kernel",
+                                  "achieved": app_bytes / (app_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                  "frac": app_bytes / (app_ms * 1e-3) / 1e9 / hbm, "us": app_ms * 1e3,
+                                  "algorithmic_bytes": app_bytes}
+        out["kv_stream_gbs"] = 2 * nk * H * D * 9 / 16 / (att_ms * 1e-3) / 1e9
+        out["attention_tflops"] = ach
+        out["e2e"] = e2e
+    out["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        est, desc = oracle_sample()
+        out["cpu_baseline"] = {"value": T_C / est, "unit": "query-tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                               "sample": desc, "est_step_s": est}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        oracle_sample(q_rows=4, quant_frac=32)
+    ts = []
+    desc = ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        est, desc = oracle_sample(q_rows=4, quant_frac=32)
+        ts.append(est)
+    wall = time.perf_counter() - t0
+    est = float(np.mean(ts))
+    v = T_C / est
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "query-tokens/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64 (CPU oracle)",
+           "data": "synthetic (same seeded inputs)", "config": {"workload": WORKLOAD, "heads": H, "head_dim": D,
+                                                                 "T_c": T_C, "n_keys": n_keys()},
+           "cpu_baseline": {"value": v, "unit": "query-tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                            "sample": desc + "; each bench step is one such sample", "wall_s": wall},
+           "e2e": {"value": v, "unit": "query-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * kvq.h -- C ABI of the B200-native NVFP4 KV-cache + fused-dequant chunk-attention library
+ * (libkvq.so), the hot path of LongLive-2.0's inference infrastructure (arxiv 2605.18739).
+ *
+ * Citations are lines of the paper's text, PAPER.md (LaTeX of arxiv 2605.18739), with the
+ * section / equation they fall in; DESIGN.md §2 lists every reading taken where the paper
+ * is silent (Z1..Z19).
+ *
+ * Conventions (all entry points):
+ *  - "dev" pointers are CUDA device pointers OWNED BY THE CALLER (in practice torch tensors);
+ *    "host" pointers are ordinary host memory.  The library owns only host metadata.
+ *    No entry point allocates device memory.
+ *  - Argument errors (bad layer, d not in {64,128}, unknown chunk, ...) are returned
+ *    synchronously as a negative kvq_status and NOTHING is launched.
+ *  - Data errors found on the device (non-finite input) are asynchronous: they are recorded
+ *    in a device status word and reported by kvq_get_status().
+ *  - All device work is ordered on the cudaStream_t passed in (passed as void* so the header
+ *    needs no CUDA include); nothing synchronizes the host except kvq_get_status().
+ *  - A cache has a single writer (kv_quantize_append); concurrent chunk_attention calls on
+ *    other streams are allowed only while no append is in flight.
+ *  - Layouts: an activation tensor [T, H, d] is row-major, row = (t, h), t-major -- the
+ *    paper's (T_c H) x d reshape of K_{l,c} (§3.2).
+ */
+#ifndef KVQ_H_
+#define KVQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KVQ_OK = 0,
+  KVQ_EINVAL = -1,      /* bad argument value or null pointer */
+  KVQ_ESHAPE = -2,      /* unsupported shape (d not 64/128, T_c not a multiple of 16, ...) */
+  KVQ_EDTYPE = -3,      /* unsupported dtype combination */
+  KVQ_ENOCHUNK = -4,    /* chunk index is neither newest+1 (append) nor newest (overwrite), or a
+                           key chunk needed by the mask is not resident */
+  KVQ_ECAPACITY = -5,   /* no free slot: every slot holds a pinned sink / window chunk */
+  KVQ_ENONFINITE = -6,  /* (async) non-finite value in an appended K or V tensor */
+  KVQ_ERANGE = -7,      /* value outside the representable range */
+  KVQ_ECUDA = -8,       /* a CUDA runtime call failed */
+  KVQ_ENCCL = -9        /* reserved for the multi-GPU exchange */
+} kvq_status;
+
+typedef enum { KVQ_BF16 = 0, KVQ_FP32 = 1, KVQ_FP16 = 2 } kvq_dtype;
+
+/* Cache geometry.  T_c = tokens_per_frame * frames_per_chunk tokens per chunk (PAPER.md:135:
+ * "Each chunk contains F_c frames and T_c = F_c L_f latent tokens").  Each chunk occupies one
+ * slot of T_pad = round_up(T_c, 128) rows so every 128-key attention tile lies in one chunk
+ * (one alpha^FP32 per tile). */
+typedef struct {
+  int32_t num_layers;
+  int32_t num_heads;        /* heads stored by THIS cache (local heads on this rank) */
+  int32_t head_dim;         /* d: 64 or 128 */
+  int32_t tokens_per_frame; /* L_f, e.g. 1560 */
+  int32_t frames_per_chunk; /* F_c, e.g. 3 */
+  int32_t sink_frames;      /* S_g of the global sink A_g, pinned, never evicted */
+  int32_t window_frames;    /* sliding window W in frames INCLUDING the current chunk (reading Z10) */
+  int32_t max_chunk_slots;  /* slots per layer; >= sink chunks + window chunks (+ shot chunks) */
+  int32_t scale_mode;       /* 0 = block scale amax/6.  Other values: KVQ_EINVAL */
+  int32_t k_smoothing;      /* 0.  K-smoothing is a later row: KVQ_EINVAL */
+} kvq_config;
+
+/* Key set of one attention call: K_eff(t) = A_g U A_s U KV_[t-W,t) U {chunk t}, deduplicated
+ * (§4.2; reading Z9: the current chunk is attended from the cache). */
+typedef struct {
+  int64_t chunk_index;       /* t: the chunk whose queries attend */
+  int32_t sink_frames;       /* S_g */
+  int32_t window_frames;     /* W in frames including the current chunk */
+  int64_t shot_start_frame;  /* A_s = (start, len) pointers; len 0 = none */
+  int64_t shot_len_frames;
+} kvq_mask;
+
+typedef struct kvq_cache kvq_cache; /* opaque; host metadata owned by the library */
+
+/* Device arena bytes for `cfg`: K/V codes (d/2 B per row), K/V E4M3 scales (d/16 B per row),
+ * the per-(layer, slot, K|V) FP32 tensor scales, amax partials and the status word.  0 on a
+ * bad config. */
+size_t kvq_cache_bytes(const kvq_config* cfg);
+
+/* Creates a cache over a caller-owned dev arena of >= kvq_cache_bytes(cfg) bytes, 256-byte
+ * aligned.  The arena is zeroed on `stream` (void* cudaStream_t).  *out receives the handle. */
+kvq_status kvq_cache_create(const kvq_config* cfg, void* dev_arena, size_t arena_bytes,
+                            void* stream, kvq_cache** out);
+kvq_status kvq_cache_destroy(kvq_cache* cache);
+/* Forget every chunk (new video); zeroes the arena on `stream`. */
+kvq_status kvq_cache_reset(kvq_cache* cache, void* stream);
+/* Re-bind the shot-level sink A_s (a prompt switch).  Moves two host
+ * pointers only; never touches cache bytes ("zero memory overhead").  Chunks
+ * overlapping [start, start+len) frames are pinned against eviction from now on. */
+kvq_status kvq_set_shot(kvq_cache* cache, int64_t shot_start_frame, int64_t shot_len_frames);
+
+/* NVFP4-quantize one chunk's K and V of layer `layer` and store them in the cache
+ * (§3.2: "reshape to (T_c H) x d and quantize independently with NVFP4";
+ * format PAPER.md:81-102 §2.2 Eq. 2, block scale PAPER.md:723-727 App. F).
+ * K, V: dev [T_c, H, d] in_dtype (KVQ_BF16 | KVQ_FP32).  Per tensor: g = RN32(amax/2688),
+ * per 16-block E4M3 scale s = E4M3(RN32(RN32(bmax/g)/6)), codes E2M1(RN32(x/RN32(dec(s) g)))
+ * (reading Z4, definition R1), packed 2 per byte, element 2k in the low nibble.
+ * chunk_index == newest+1 appends (evicting chunks outside sinks U window); == newest
+ * overwrites (a denoising step re-writes the in-progress chunk); the first append of a layer
+ * must be chunk 0 or any index after kvq_cache_reset.  Anything else: KVQ_ENOCHUNK.
+ * Stream-ordered; no host synchronization.  Non-finite input: the chunk is left undefined
+ * and KVQ_ENONFINITE is reported by kvq_get_status(). */
+kvq_status kv_quantize_append(kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                              const void* K, const void* V, kvq_dtype in_dtype, void* stream);
+
+/* As kv_quantize_append, but the tensor amax of K and V is supplied by the caller as two
+ * floats in device memory (dev_amax_kv[0] = amax(K), [1] = amax(V)) -- used after the
+ * Ulysses exchange, where K/V hold only this rank's heads but alpha^FP32 is taken over all
+ * heads (reading Z2/Z18). */
+kvq_status kv_quantize_append_amax(kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                                   const void* K, const void* V, kvq_dtype in_dtype,
+                                   const float* dev_amax_kv, void* stream);
+
+/* Chunk attention of chunk t's queries over the quantized cache with dequantization fused
+ * into the kernel (§3.2; K_eff PAPER.md:249; attention PAPER.md:187):
+ *   O[i,h,:] = softmax_j( Q[i,h,:] . K^[j,h,:] * scale ) V^[j,h,:],  j in K_eff(t)
+ * with K^, V^ = dec(code) dec(s) g (Eq. 2).  Q: dev [T_c, H, d] q_dtype (BF16 | FP32);
+ * O: dev [T_c, H, d] out_dtype (BF16 = the product, FP32 = parity mode).  softmax_scale <= 0
+ * means 1/sqrt(d).  Every key chunk of K_eff must be resident (else KVQ_ENOCHUNK). */
+kvq_status chunk_attention(kvq_cache* cache, int32_t layer, const void* Q, kvq_dtype q_dtype,
+                           const kvq_mask* mask, float softmax_scale, void* O,
+                           kvq_dtype out_dtype, void* stream);
+
+/* Checking: dequantize one resident chunk to dev [T_c, H, d]: FP32 = RN32(dec(c) dec(s) g)
+ * (Eq. 2), BF16 = RN_bf16 of that. */
+kvq_status kv_dequantize(const kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                         void* K_out, void* V_out, kvq_dtype out_dtype, void* stream);
+
+/* Canonical bytes of one resident chunk for bit-exact parity, rows (t, h) t-major:
+ * codes dev [T_c*H, d/2] u8, scales dev [T_c*H, d/16] u8, g dev fp32[1], for K and V. */
+kvq_status kv_export_chunk(const kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                           void* codes_k, void* scales_k, float* g_k,
+                           void* codes_v, void* scales_v, float* g_v, void* stream);
+
+/* Bytes of resident NVFP4 K/V payload (codes + scales + tensor scales) over all layers'
+ * resident chunks -- the footprint report for PAPER.md:146's "close to 3.6x". */
+size_t kvq_resident_bytes(const kvq_cache* cache);
+/* Number of resident chunks of `layer` (host metadata). */
+int32_t kvq_resident_chunks(const kvq_cache* cache, int32_t layer);
+
+/* Bench-only (not the product path): the paper's unfused design -- reconstruct K_eff into a
+ * contiguous bf16 buffer dev [n_keys, H, d] (the "customized parallel dequantization kernel",
+ * PAPER.md:146) -- and attention over caller-provided bf16 K/V (the same kernel family with
+ * no dequantization; BASELINE.json config 4 "NVFP4 vs bf16 KV").  *n_keys (host) receives
+ * |K_eff|; pass K_out = V_out = NULL to query it only. */
+kvq_status kv_dequantize_window(const kvq_cache* cache, int32_t layer, const kvq_mask* mask,
+                                void* K_out, void* V_out, int64_t* n_keys, void* stream);
+kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, int32_t T_q,
+                                  int64_t n_keys, int32_t H, int32_t d, float softmax_scale,
+                                  void* O, kvq_dtype out_dtype, void* stream);
+
+/* Asynchronous data errors: synchronizes `stream`, returns the first recorded error (or
+ * KVQ_OK) and the first offending flat element index (K: index into K, V: T_c*H*d + index),
+ * then clears it. */
+kvq_status kvq_get_status(kvq_cache* cache, void* stream, int64_t* first_bad_index);
+const char* kvq_strerror(kvq_status s);
+
+/* ---------------------------------------------------------------------------------------
+ * Head-sharded (Ulysses) exchange, PAPER.md:556-564 (App. C) and PAPER.md:640-650 (App. D):
+ * z^(p) in R^{L/P x H x d} --All-to-All--> R^{L x H/P x d}; a second All-to-All restores the
+ * sequence-sharded layout.  The collective itself is NCCL (torch.distributed); these kernels
+ * are the compute around it.  Heads are split contiguously, the first H % P ranks get one more
+ * (12 heads on 8 ranks: 2,2,2,2,1,1,1,1). */
+void kvq_head_partition(int32_t H, int32_t P, int32_t rank, int32_t* h0, int32_t* h1);
+
+/* Bytes this rank sends to destination `dst` for Q|K|V (= bytes it receives from any source
+ * when dst == this rank): 3 * Ts * H_dst * d * esize + 16 (trailer: amax(K), amax(V) of the
+ * sender's sequence shard as fp32, then 8 pad bytes). */
+size_t kvq_ulysses_qkv_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst,
+                             kvq_dtype dtype);
+
+/* Pack this rank's sequence shard Q, K, V dev [Ts, H, d] into the all-to-allv send buffer:
+ * for destination p, one contiguous segment [3][Ts][H_p][d] + trailer, segments in rank
+ * order.  Also computes the shard's amax(K), amax(V) into every trailer.
+ * dev_scratch: >= 8192 bytes of caller-owned device scratch. */
+kvq_status kvq_ulysses_pack_qkv(const void* Q, const void* K, const void* V, kvq_dtype dtype,
+                                int32_t Ts, int32_t H, int32_t d, int32_t P, void* send_buf,
+                                void* dev_scratch, void* stream);
+
+/* Unpack what this rank (owning H_r heads) received -- P segments [3][Ts][H_r][d] + trailer
+ * from sources 0..P-1 -- into contiguous Q, K, V dev [P*Ts, H_r, d] and the global
+ * amax_kv dev fp32[2] = max over sources (reading Z18: codes equal the 1-GPU run). */
+kvq_status kvq_ulysses_unpack_qkv(const void* recv_buf, kvq_dtype dtype, int32_t Ts,
+                                  int32_t H_r, int32_t d, int32_t P, void* Q, void* K, void* V,
+                                  float* dev_amax_kv, void* stream);
+
+/* After attention: O_local dev [P*Ts, H_r, d] is sent as P contiguous token blocks (equal
+ * splits, no pack needed).  Unpack the received P blocks [Ts][H_p][d] (p = 0..P-1, head
+ * counts from kvq_head_partition) into this rank's output shard dev [Ts, H, d]. */
+kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t Ts, int32_t H,
+                                int32_t d, int32_t P, void* O_shard, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVQ_H_ */

@@ -1,0 +1,24 @@
+/*
+ * kvq_debug.h -- diagnostic entry points of libkvq.so (not the product path).
+ *
+ * kvq_debug_probe runs the hardware NVFP4 conversions used by the kernels element by element so
+ * tests can compare them with the float64 oracle's codecs (PAPER.md:719 E2M1 value set,
+ * PAPER.md:102 E4M3 max 448; readings Z3, Z6-Z8 of DESIGN.md):
+ *   which = 0: E2M1 encode, dev_in fp32[2n] -> dev_out u8[2n] (one code per element;
+ *              cvt.rn.satfinite.e2m1x2.f32, element 2k taken from the low nibble)
+ *   which = 1: E4M3 encode of non-negative values, fp32[n] -> u8[n] (cvt.rn.satfinite.e4m3x2.f32)
+ *   which = 2: E2M1 decode, u8[n] (two codes per byte) -> fp32[2n], low nibble first
+ *   which = 3: E4M3 decode, u8[n] -> fp32[n]
+ * Returns KVQ_EINVAL on a bad `which` or null pointer; stream-ordered on `stream`.
+ */
+#ifndef KVQ_DEBUG_H_
+#define KVQ_DEBUG_H_
+#include "kvq.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+kvq_status kvq_debug_probe(int32_t which, const void* dev_in, void* dev_out, int64_t n, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

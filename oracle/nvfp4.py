@@ -68,18 +68,20 @@ def e2m1_encode(x):
     negatives that round to 0 give code 8).
     """
     x = np.asarray(x, dtype=np.float64)
-    a = np.minimum(np.abs(x), M_FP4)[..., None]              # saturation: RNE(|x| > 6) -> 6
-    dist = np.abs(a - E2M1_MAGNITUDES)                       # [..., 8], exact in f64
-    best = dist.min(axis=-1, keepdims=True)
-    is_best = dist == best
+    flat = x.reshape(-1)
+    out = np.empty(flat.shape, dtype=np.uint8)
     even = (np.arange(8) % 2) == 0
-    # prefer the even code among ties; otherwise the unique nearest
-    choose_even = (is_best & even).any(axis=-1)
-    idx_even = np.argmax(is_best & even, axis=-1)
-    idx_any = np.argmax(is_best, axis=-1)
-    mag_code = np.where(choose_even, idx_even, idx_any)
-    sign = np.signbit(x).astype(np.int64)
-    return (mag_code + 8 * sign).astype(np.uint8)
+    step = 1 << 20                                           # bounds memory only
+    for i in range(0, flat.size, step):
+        xs = flat[i:i + step]
+        a = np.minimum(np.abs(xs), M_FP4)[:, None]           # saturation: RNE(|x| > 6) -> 6
+        dist = np.abs(a - E2M1_MAGNITUDES)                   # [n, 8], exact in f64
+        is_best = dist == dist.min(axis=-1, keepdims=True)
+        # prefer the even code among ties; otherwise the unique nearest
+        choose_even = (is_best & even).any(axis=-1)
+        mag_code = np.where(choose_even, np.argmax(is_best & even, axis=-1), np.argmax(is_best, axis=-1))
+        out[i:i + step] = mag_code + 8 * np.signbit(xs)
+    return out.reshape(x.shape)
 
 
 # ----------------------------------------------------------------------------- E4M3

@@ -1,0 +1,520 @@
+// api.cpp -- host side of the C ABI (include/kvq.h): argument validation, the chunk -> slot map
+// with sink / window eviction, K_eff resolution into cache segments, and kernel launches.
+// No device memory is allocated here; the caller owns the arena.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+#include <set>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/kvq.h"
+#include "../../include/kvq_debug.h"
+#include "internal.h"
+
+using namespace kvq;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  int64_t T_c, T_pad, rows_per_head;  // rows_per_head = slots * T_pad
+  size_t codes_bytes, scales_bytes;   // per tensor (K or V), all layers
+  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, total;
+};
+
+bool valid_cfg(const kvq_config* c) {
+  if (!c) return false;
+  if (c->num_layers <= 0 || c->num_heads <= 0) return false;
+  if (c->head_dim != 64 && c->head_dim != 128) return false;
+  if (c->tokens_per_frame <= 0 || c->frames_per_chunk <= 0) return false;
+  if (c->sink_frames < 0 || c->window_frames < c->frames_per_chunk) return false;
+  if (c->max_chunk_slots <= 0) return false;
+  if (c->scale_mode != 0 || c->k_smoothing != 0) return false;
+  int64_t Tc = (int64_t)c->tokens_per_frame * c->frames_per_chunk;
+  if (Tc > (1 << 24)) return false;
+  return true;
+}
+
+Layout make_layout(const kvq_config* c) {
+  Layout L{};
+  L.T_c = (int64_t)c->tokens_per_frame * c->frames_per_chunk;
+  L.T_pad = (L.T_c + kTileKeys - 1) / kTileKeys * kTileKeys;
+  L.rows_per_head = (int64_t)c->max_chunk_slots * L.T_pad;
+  const int64_t rows = (int64_t)c->num_layers * c->num_heads * L.rows_per_head;
+  L.codes_bytes = align_up((size_t)rows * (c->head_dim / 2), kAlign);
+  L.scales_bytes = align_up((size_t)rows * (c->head_dim / 16), kAlign);
+  size_t off = 0;
+  L.off_codes[0] = off; off += L.codes_bytes;
+  L.off_codes[1] = off; off += L.codes_bytes;
+  L.off_scales[0] = off; off += L.scales_bytes;
+  L.off_scales[1] = off; off += L.scales_bytes;
+  L.off_g = off; off += align_up((size_t)c->num_layers * c->max_chunk_slots * 2 * sizeof(float), kAlign);
+  L.off_partials = off; off += align_up(2 * kNumPartials * sizeof(uint32_t), kAlign);
+  L.off_status = off; off += align_up(sizeof(DevStatus), kAlign);
+  L.total = off;
+  return L;
+}
+
+struct LayerState {
+  int64_t newest = -1;
+  std::map<int64_t, int> slot_of;  // resident chunk -> slot
+  std::vector<int64_t> chunk_in;   // slot -> chunk (-1 free)
+};
+
+}  // namespace
+
+struct kvq_cache {
+  kvq_config cfg;
+  Layout L;
+  uint8_t* arena;
+  std::vector<LayerState> layers;
+  int64_t shot_start = 0, shot_len = 0;
+};
+
+namespace {
+
+kvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? KVQ_OK : KVQ_ECUDA; }
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+uint8_t* codes_base(const kvq_cache* c, int t, int layer) {
+  return c->arena + c->L.off_codes[t] + (size_t)layer * c->cfg.num_heads * c->L.rows_per_head * (c->cfg.head_dim / 2);
+}
+uint8_t* scales_base(const kvq_cache* c, int t, int layer) {
+  return c->arena + c->L.off_scales[t] + (size_t)layer * c->cfg.num_heads * c->L.rows_per_head * (c->cfg.head_dim / 16);
+}
+float* g_base(const kvq_cache* c, int layer) {
+  return reinterpret_cast<float*>(c->arena + c->L.off_g) + (size_t)layer * c->cfg.max_chunk_slots * 2;
+}
+DevStatus* status_ptr(const kvq_cache* c) { return reinterpret_cast<DevStatus*>(c->arena + c->L.off_status); }
+
+kvq_status reset_device(kvq_cache* c, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(c->arena, 0, c->L.total, st);
+  if (e != cudaSuccess) return KVQ_ECUDA;
+  DevStatus init{0, 0, ~0ull};
+  // status word: code 0, first_bad = max (a small H2D copy from a static host value)
+  static DevStatus s_init = init;
+  e = cudaMemcpyAsync(status_ptr(c), &s_init, sizeof(DevStatus), cudaMemcpyHostToDevice, st);
+  return cuda_status(e);
+}
+
+// Frames of K_eff(t) (readings Z9-Z11) -> sorted distinct chunk-local token ranges
+// in logical token coordinates.
+std::vector<std::pair<int64_t, int64_t>> key_token_ranges(int64_t t, int64_t fc, int64_t tpf, int64_t sink,
+                                                          int64_t window, int64_t shot0, int64_t shotn) {
+  const int64_t f_end = (t + 1) * fc;
+  std::vector<std::pair<int64_t, int64_t>> fr;  // frame intervals
+  fr.push_back({0, std::min(sink, f_end)});
+  if (shotn > 0) fr.push_back({std::max<int64_t>(shot0, 0), std::min(shot0 + shotn, f_end)});
+  fr.push_back({std::max<int64_t>(0, f_end - window), f_end});
+  fr.push_back({f_end - fc, f_end});
+  std::sort(fr.begin(), fr.end());
+  std::vector<std::pair<int64_t, int64_t>> out;
+  for (auto& iv : fr) {
+    if (iv.second <= iv.first) continue;
+    if (!out.empty() && iv.first <= out.back().second) out.back().second = std::max(out.back().second, iv.second);
+    else out.push_back(iv);
+  }
+  for (auto& iv : out) {
+    iv.first *= tpf;
+    iv.second *= tpf;
+  }
+  return out;
+}
+
+// chunks touched by the ranges
+std::set<int64_t> chunks_of(const std::vector<std::pair<int64_t, int64_t>>& r, int64_t Tc) {
+  std::set<int64_t> s;
+  for (auto& iv : r)
+    for (int64_t c = iv.first / Tc; c * Tc < iv.second; ++c) s.insert(c);
+  return s;
+}
+
+kvq_status resolve_segments(const kvq_cache* c, int layer, const kvq_mask* m, std::vector<AttnSeg>& segs) {
+  const LayerState& ls = c->layers[layer];
+  auto ranges = key_token_ranges(m->chunk_index, c->cfg.frames_per_chunk, c->cfg.tokens_per_frame, m->sink_frames,
+                                 m->window_frames, m->shot_start_frame, m->shot_len_frames);
+  const int64_t Tc = c->L.T_c;
+  segs.clear();
+  for (auto& iv : ranges) {
+    int64_t tok = iv.first;
+    while (tok < iv.second) {
+      const int64_t ch = tok / Tc;
+      const int64_t end = std::min(iv.second, (ch + 1) * Tc);
+      auto it = ls.slot_of.find(ch);
+      if (it == ls.slot_of.end()) return KVQ_ENOCHUNK;
+      if ((int)segs.size() >= kMaxSegs) return KVQ_EINVAL;
+      segs.push_back(AttnSeg{it->second, (int32_t)(tok - ch * Tc), (int32_t)(end - ch * Tc)});
+      tok = end;
+    }
+  }
+  return KVQ_OK;
+}
+
+kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K, const void* V, kvq_dtype dt,
+                       const float* ext_amax, void* stream) {
+  if (!c || !K || !V) return KVQ_EINVAL;
+  if (layer < 0 || layer >= c->cfg.num_layers || chunk < 0) return KVQ_EINVAL;
+  if (dt != KVQ_BF16 && dt != KVQ_FP32) return KVQ_EDTYPE;
+  LayerState& ls = c->layers[layer];
+  int slot = -1;
+  if (ls.newest >= 0 && chunk == ls.newest) {
+    slot = ls.slot_of.at(chunk);  // denoising re-write of the in-progress chunk
+  } else if (ls.newest < 0 || chunk == ls.newest + 1) {
+    // evict chunks that K_eff of this and later steps can no longer reach: keep the global sink,
+    // the bound shot sink and the window ending at the new chunk
+    auto keep = chunks_of(key_token_ranges(chunk, c->cfg.frames_per_chunk, 1, c->cfg.sink_frames,
+                                           c->cfg.window_frames, c->shot_start, c->shot_len),
+                          c->cfg.frames_per_chunk);
+    for (auto it = ls.slot_of.begin(); it != ls.slot_of.end();) {
+      if (!keep.count(it->first)) {
+        ls.chunk_in[it->second] = -1;
+        it = ls.slot_of.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    for (int s = 0; s < c->cfg.max_chunk_slots; ++s)
+      if (ls.chunk_in[s] < 0) { slot = s; break; }
+    if (slot < 0) return KVQ_ECAPACITY;
+  } else {
+    return KVQ_ENOCHUNK;
+  }
+  const int H = c->cfg.num_heads, d = c->cfg.head_dim;
+  const int64_t rows = c->L.T_c * H;
+  cudaStream_t st = S(stream);
+  uint32_t* partials = reinterpret_cast<uint32_t*>(c->arena + c->L.off_partials);
+  if (!ext_amax) {
+    cudaError_t e = launch_amax(K, V, dt == KVQ_BF16 ? DT_BF16 : DT_FP32, rows * d, partials, status_ptr(c), st);
+    if (e != cudaSuccess) return KVQ_ECUDA;
+  }
+  QuantParams p{};
+  p.x[0] = K;
+  p.x[1] = V;
+  p.dtype = dt == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.rows = (int)rows;
+  p.H = H;
+  p.d = d;
+  for (int t = 0; t < 2; ++t) {
+    p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
+    p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);
+  }
+  p.head_stride_rows = c->L.rows_per_head;
+  p.g_out = g_base(c, layer) + slot * 2;
+  p.partials = ext_amax ? nullptr : partials;
+  p.ext_amax = ext_amax;
+  p.status = status_ptr(c);
+  cudaError_t e = launch_quantize(p, st);
+  if (e != cudaSuccess) return KVQ_ECUDA;
+  ls.slot_of[chunk] = slot;
+  ls.chunk_in[slot] = chunk;
+  ls.newest = chunk;
+  return KVQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t kvq_cache_bytes(const kvq_config* cfg) {
+  if (!valid_cfg(cfg)) return 0;
+  return make_layout(cfg).total;
+}
+
+kvq_status kvq_cache_create(const kvq_config* cfg, void* dev_arena, size_t arena_bytes, void* stream,
+                            kvq_cache** out) {
+  if (!out) return KVQ_EINVAL;
+  *out = nullptr;
+  if (!valid_cfg(cfg)) return (cfg && (cfg->head_dim != 64 && cfg->head_dim != 128)) ? KVQ_ESHAPE : KVQ_EINVAL;
+  if (!dev_arena || (reinterpret_cast<uintptr_t>(dev_arena) % kAlign) != 0) return KVQ_EINVAL;
+  Layout L = make_layout(cfg);
+  if (arena_bytes < L.total) return KVQ_EINVAL;
+  kvq_cache* c = new (std::nothrow) kvq_cache();
+  if (!c) return KVQ_EINVAL;
+  c->cfg = *cfg;
+  c->L = L;
+  c->arena = static_cast<uint8_t*>(dev_arena);
+  c->layers.resize(cfg->num_layers);
+  for (auto& ls : c->layers) ls.chunk_in.assign(cfg->max_chunk_slots, -1);
+  kvq_status s = reset_device(c, S(stream));
+  if (s != KVQ_OK) {
+    delete c;
+    return s;
+  }
+  *out = c;
+  return KVQ_OK;
+}
+
+kvq_status kvq_cache_destroy(kvq_cache* cache) {
+  delete cache;
+  return KVQ_OK;
+}
+
+kvq_status kvq_cache_reset(kvq_cache* c, void* stream) {
+  if (!c) return KVQ_EINVAL;
+  for (auto& ls : c->layers) {
+    ls.newest = -1;
+    ls.slot_of.clear();
+    ls.chunk_in.assign(c->cfg.max_chunk_slots, -1);
+  }
+  c->shot_start = c->shot_len = 0;
+  return reset_device(c, S(stream));
+}
+
+kvq_status kvq_set_shot(kvq_cache* c, int64_t shot_start_frame, int64_t shot_len_frames) {
+  if (!c || shot_start_frame < 0 || shot_len_frames < 0) return KVQ_EINVAL;
+  c->shot_start = shot_start_frame;
+  c->shot_len = shot_len_frames;
+  return KVQ_OK;
+}
+
+kvq_status kv_quantize_append(kvq_cache* c, int32_t layer, int64_t chunk, const void* K, const void* V,
+                              kvq_dtype dt, void* stream) {
+  return append_impl(c, layer, chunk, K, V, dt, nullptr, stream);
+}
+
+kvq_status kv_quantize_append_amax(kvq_cache* c, int32_t layer, int64_t chunk, const void* K, const void* V,
+                                   kvq_dtype dt, const float* dev_amax_kv, void* stream) {
+  if (!dev_amax_kv) return KVQ_EINVAL;
+  return append_impl(c, layer, chunk, K, V, dt, dev_amax_kv, stream);
+}
+
+kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
+                           float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+  if (!c || !Q || !O || !mask) return KVQ_EINVAL;
+  if (layer < 0 || layer >= c->cfg.num_layers || mask->chunk_index < 0) return KVQ_EINVAL;
+  if (mask->sink_frames < 0 || mask->window_frames < 0 || mask->shot_len_frames < 0) return KVQ_EINVAL;
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  AttnParams p{};
+  std::vector<AttnSeg> segs;
+  kvq_status s = resolve_segments(c, layer, mask, segs);
+  if (s != KVQ_OK) return s;
+  p.nseg = (int)segs.size();
+  std::copy(segs.begin(), segs.end(), p.seg);
+  const int d = c->cfg.head_dim;
+  p.Q = Q;
+  p.q_dtype = q_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.O = O;
+  p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.codes_k = codes_base(c, 0, layer);
+  p.codes_v = codes_base(c, 1, layer);
+  p.scales_k = scales_base(c, 0, layer);
+  p.scales_v = scales_base(c, 1, layer);
+  p.g = g_base(c, layer);
+  p.head_stride_rows = c->L.rows_per_head;
+  p.T_pad = (int)c->L.T_pad;
+  p.Tq = (int)c->L.T_c;
+  p.H = c->cfg.num_heads;
+  p.d = d;
+  const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
+  p.scale_log2 = sc * 1.4426950408889634f;
+  return cuda_status(launch_attention(p, true, S(stream)));
+}
+
+kvq_status kv_dequantize(const kvq_cache* c, int32_t layer, int64_t chunk, void* K_out, void* V_out,
+                         kvq_dtype out_dtype, void* stream) {
+  if (!c || !K_out || !V_out || layer < 0 || layer >= c->cfg.num_layers) return KVQ_EINVAL;
+  if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  auto it = c->layers[layer].slot_of.find(chunk);
+  if (it == c->layers[layer].slot_of.end()) return KVQ_ENOCHUNK;
+  const int slot = it->second, d = c->cfg.head_dim;
+  DequantParams p{};
+  for (int t = 0; t < 2; ++t) {
+    p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
+    p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);
+  }
+  p.g = g_base(c, layer) + slot * 2;
+  p.head_stride_rows = c->L.rows_per_head;
+  p.T = (int)c->L.T_c;
+  p.H = c->cfg.num_heads;
+  p.d = d;
+  p.out[0] = K_out;
+  p.out[1] = V_out;
+  p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  return cuda_status(launch_dequantize(p, S(stream)));
+}
+
+kvq_status kv_export_chunk(const kvq_cache* c, int32_t layer, int64_t chunk, void* codes_k, void* scales_k,
+                           float* g_k, void* codes_v, void* scales_v, float* g_v, void* stream) {
+  if (!c || layer < 0 || layer >= c->cfg.num_layers) return KVQ_EINVAL;
+  if (!codes_k || !scales_k || !g_k || !codes_v || !scales_v || !g_v) return KVQ_EINVAL;
+  auto it = c->layers[layer].slot_of.find(chunk);
+  if (it == c->layers[layer].slot_of.end()) return KVQ_ENOCHUNK;
+  const int slot = it->second, d = c->cfg.head_dim;
+  ExportParams p{};
+  for (int t = 0; t < 2; ++t) {
+    p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
+    p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);
+  }
+  p.g = g_base(c, layer) + slot * 2;
+  p.head_stride_rows = c->L.rows_per_head;
+  p.T = (int)c->L.T_c;
+  p.H = c->cfg.num_heads;
+  p.d = d;
+  p.codes_out[0] = static_cast<uint8_t*>(codes_k);
+  p.codes_out[1] = static_cast<uint8_t*>(codes_v);
+  p.scales_out[0] = static_cast<uint8_t*>(scales_k);
+  p.scales_out[1] = static_cast<uint8_t*>(scales_v);
+  p.g_out[0] = g_k;
+  p.g_out[1] = g_v;
+  return cuda_status(launch_export(p, S(stream)));
+}
+
+size_t kvq_resident_bytes(const kvq_cache* c) {
+  if (!c) return 0;
+  size_t n = 0;
+  const size_t rows = (size_t)c->L.T_c * c->cfg.num_heads;
+  const size_t per_chunk = 2 * (rows * (c->cfg.head_dim / 2) + rows * (c->cfg.head_dim / 16) + sizeof(float));
+  for (auto& ls : c->layers) n += ls.slot_of.size() * per_chunk;
+  return n;
+}
+
+int32_t kvq_resident_chunks(const kvq_cache* c, int32_t layer) {
+  if (!c || layer < 0 || layer >= c->cfg.num_layers) return -1;
+  return (int32_t)c->layers[layer].slot_of.size();
+}
+
+kvq_status kv_dequantize_window(const kvq_cache* c, int32_t layer, const kvq_mask* mask, void* K_out, void* V_out,
+                                int64_t* n_keys, void* stream) {
+  if (!c || !mask || !n_keys || layer < 0 || layer >= c->cfg.num_layers) return KVQ_EINVAL;
+  std::vector<AttnSeg> segs;
+  kvq_status s = resolve_segments(c, layer, mask, segs);
+  if (s != KVQ_OK) return s;
+  int64_t n = 0;
+  for (auto& sg : segs) n += sg.end - sg.begin;
+  *n_keys = n;
+  if (!K_out && !V_out) return KVQ_OK;
+  if (!K_out || !V_out) return KVQ_EINVAL;
+  const int d = c->cfg.head_dim;
+  DequantParams p{};
+  p.codes[0] = codes_base(c, 0, layer);
+  p.codes[1] = codes_base(c, 1, layer);
+  p.scales[0] = scales_base(c, 0, layer);
+  p.scales[1] = scales_base(c, 1, layer);
+  p.g = g_base(c, layer);
+  p.head_stride_rows = c->L.rows_per_head;
+  p.T = (int)c->L.T_pad;
+  p.H = c->cfg.num_heads;
+  p.d = d;
+  p.out_dtype = DT_BF16;
+  return cuda_status(launch_dequant_window(p, segs.data(), (int)segs.size(), K_out, V_out, S(stream)));
+}
+
+kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, int32_t T_q, int64_t n_keys, int32_t H,
+                                  int32_t d, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+  if (!Q || !K || !V || !O || T_q <= 0 || n_keys <= 0 || H <= 0) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (n_keys > INT_MAX) return KVQ_ESHAPE;
+  if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  AttnParams p{};
+  p.Q = Q;
+  p.q_dtype = DT_BF16;
+  p.O = O;
+  p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.Kb = K;
+  p.Vb = V;
+  p.Tq = T_q;
+  p.H = H;
+  p.d = d;
+  p.nseg = 1;
+  p.seg[0] = AttnSeg{0, 0, (int32_t)n_keys};
+  const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
+  p.scale_log2 = sc * 1.4426950408889634f;
+  return cuda_status(launch_attention(p, false, S(stream)));
+}
+
+kvq_status kvq_get_status(kvq_cache* c, void* stream, int64_t* first_bad_index) {
+  if (!c) return KVQ_EINVAL;
+  cudaStream_t st = S(stream);
+  DevStatus h{};
+  if (cudaMemcpyAsync(&h, status_ptr(c), sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess) return KVQ_ECUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return KVQ_ECUDA;
+  if (first_bad_index) *first_bad_index = h.first_bad == ~0ull ? -1 : (int64_t)h.first_bad;
+  if (h.code != 0) {
+    static DevStatus s_init{0, 0, ~0ull};
+    if (cudaMemcpyAsync(status_ptr(c), &s_init, sizeof(DevStatus), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return KVQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return KVQ_ECUDA;
+  }
+  return (kvq_status)h.code;
+}
+
+const char* kvq_strerror(kvq_status s) {
+  switch (s) {
+    case KVQ_OK: return "ok";
+    case KVQ_EINVAL: return "invalid argument";
+    case KVQ_ESHAPE: return "unsupported shape";
+    case KVQ_EDTYPE: return "unsupported dtype";
+    case KVQ_ENOCHUNK: return "chunk not appendable or not resident";
+    case KVQ_ECAPACITY: return "no free cache slot";
+    case KVQ_ENONFINITE: return "non-finite input";
+    case KVQ_ERANGE: return "value out of range";
+    case KVQ_ECUDA: return "CUDA error";
+    case KVQ_ENCCL: return "NCCL error";
+  }
+  return "unknown status";
+}
+
+// ----------------------------------------------------------------------------- Ulysses
+void kvq_head_partition(int32_t H, int32_t P, int32_t rank, int32_t* h0, int32_t* h1) {
+  if (P <= 0 || rank < 0 || rank >= P || H < 0) {
+    if (h0) *h0 = 0;
+    if (h1) *h1 = 0;
+    return;
+  }
+  const int32_t base = H / P, rem = H % P;
+  const int32_t a = rank * base + std::min(rank, rem);
+  if (h0) *h0 = a;
+  if (h1) *h1 = a + base + (rank < rem ? 1 : 0);
+}
+
+static size_t esize(kvq_dtype d) { return d == KVQ_FP32 ? 4 : 2; }
+
+size_t kvq_ulysses_qkv_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst, kvq_dtype dtype) {
+  int32_t h0, h1;
+  kvq_head_partition(H, P, dst, &h0, &h1);
+  return 3 * (size_t)Ts * (h1 - h0) * d * esize(dtype) + 16;
+}
+
+kvq_status kvq_ulysses_pack_qkv(const void* Q, const void* K, const void* V, kvq_dtype dtype, int32_t Ts, int32_t H,
+                                int32_t d, int32_t P, void* send_buf, void* dev_scratch, void* stream) {
+  if (!Q || !K || !V || !send_buf || !dev_scratch || Ts <= 0 || H <= 0 || P <= 0 || P > 64) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  return cuda_status(launch_ulysses_pack(Q, K, V, dtype == KVQ_BF16 ? DT_BF16 : DT_FP32, Ts, H, d, P,
+                                         static_cast<uint8_t*>(send_buf), static_cast<uint32_t*>(dev_scratch),
+                                         S(stream)));
+}
+
+kvq_status kvq_ulysses_unpack_qkv(const void* recv_buf, kvq_dtype dtype, int32_t Ts, int32_t H_r, int32_t d, int32_t P,
+                                  void* Q, void* K, void* V, float* dev_amax_kv, void* stream) {
+  if (!recv_buf || !Q || !K || !V || !dev_amax_kv || Ts <= 0 || H_r <= 0 || P <= 0 || P > 64) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  return cuda_status(launch_ulysses_unpack_qkv(static_cast<const uint8_t*>(recv_buf), dtype == KVQ_BF16 ? DT_BF16 : DT_FP32,
+                                               Ts, H_r, d, P, Q, K, V, dev_amax_kv, S(stream)));
+}
+
+kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t Ts, int32_t H, int32_t d, int32_t P,
+                                void* O_shard, void* stream) {
+  if (!recv_buf || !O_shard || Ts <= 0 || H <= 0 || P <= 0 || P > 64) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  return cuda_status(launch_ulysses_unpack_o(static_cast<const uint8_t*>(recv_buf), dtype == KVQ_BF16 ? DT_BF16 : DT_FP32,
+                                             Ts, H, d, P, O_shard, S(stream)));
+}
+
+// Debug probe entry point (declared in include/kvq_debug.h)
+kvq_status kvq_debug_probe(int32_t which, const void* dev_in, void* dev_out, int64_t n, void* stream) {
+  if (!dev_in || !dev_out || n < 0 || which < 0 || which > 3) return KVQ_EINVAL;
+  return cuda_status(launch_probe(which, dev_in, dev_out, n, S(stream)));
+}
+
+}  // extern "C"

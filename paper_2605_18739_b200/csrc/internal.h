@@ -1,0 +1,103 @@
+// internal.h -- launch interfaces between the host C-ABI layer (api.cpp) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kvq {
+
+constexpr int kTileKeys = 128;     // keys per attention tile; slots are padded to a multiple
+constexpr int kNumPartials = 592;  // amax partials per tensor (4 x 148 SMs)
+constexpr int kMaxSegs = 48;       // key segments per attention call
+
+enum DType : int { DT_BF16 = 0, DT_FP32 = 1, DT_FP16 = 2 };
+
+// Device status word (in the arena): code (0 = ok), then first bad flat index.
+struct DevStatus {
+  int32_t code;
+  int32_t pad;
+  unsigned long long first_bad;
+};
+
+struct QuantParams {
+  const void* x[2];          // K, V: [rows = T_c*H, d] t-major
+  int dtype;                 // DT_BF16 | DT_FP32
+  int rows, H, d;
+  uint8_t* codes[2];         // slot base for head 0, rows of d/2 bytes
+  uint8_t* scales[2];        // slot base for head 0, rows of d/16 bytes
+  int64_t head_stride_rows;  // rows between heads (= slots * T_pad)
+  float* g_out;              // [2]: K, V tensor scales of this (layer, slot)
+  const uint32_t* partials;  // [2][kNumPartials] amax bit patterns, or null
+  const float* ext_amax;     // [2] caller-supplied amax (Ulysses), or null
+  DevStatus* status;
+};
+
+struct DequantParams {
+  const uint8_t* codes[2];
+  const uint8_t* scales[2];
+  const float* g;            // [2]
+  int64_t head_stride_rows;
+  int T, H, d;
+  void* out[2];              // [T, H, d]
+  int out_dtype;             // DT_FP32 | DT_BF16
+};
+
+struct ExportParams {
+  const uint8_t* codes[2];
+  const uint8_t* scales[2];
+  const float* g;
+  int64_t head_stride_rows;
+  int T, H, d;
+  uint8_t* codes_out[2];
+  uint8_t* scales_out[2];
+  float* g_out[2];
+};
+
+struct AttnSeg {
+  int32_t slot;   // cache slot (bf16kv mode: ignored)
+  int32_t begin;  // first key row inside the slot
+  int32_t end;    // one past the last key row
+};
+
+struct AttnParams {
+  const void* Q;             // [Tq, H, d]
+  int q_dtype;               // DT_BF16 | DT_FP32
+  void* O;                   // [Tq, H, d]
+  int out_dtype;             // DT_BF16 | DT_FP32
+  // NVFP4 cache (layer base, head 0, slot 0)
+  const uint8_t* codes_k;
+  const uint8_t* codes_v;
+  const uint8_t* scales_k;
+  const uint8_t* scales_v;
+  const float* g;            // g[slot*2 + {0,1}]
+  int64_t head_stride_rows;  // slots * T_pad
+  int T_pad;                 // rows per slot (multiple of 128)
+  // bf16 KV mode: K, V [n_keys, H, d]
+  const void* Kb;
+  const void* Vb;
+  int Tq, H, d;
+  float scale_log2;          // softmax_scale * log2(e)
+  int nseg;
+  AttnSeg seg[kMaxSegs];
+};
+
+cudaError_t launch_amax(const void* K, const void* V, int dtype, int64_t n, uint32_t* partials,
+                        DevStatus* status, cudaStream_t st);
+cudaError_t launch_quantize(const QuantParams& p, cudaStream_t st);
+cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t st);
+cudaError_t launch_export(const ExportParams& p, cudaStream_t st);
+cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st);
+cudaError_t launch_dequant_window(const DequantParams& base, const AttnSeg* segs, int nseg, void* Kout,
+                                  void* Vout, cudaStream_t st);
+
+// Ulysses exchange kernels
+cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int dtype, int Ts, int H, int d,
+                                int P, uint8_t* send, uint32_t* scratch, cudaStream_t st);
+cudaError_t launch_ulysses_unpack_qkv(const uint8_t* recv, int dtype, int Ts, int Hr, int d, int P, void* Q,
+                                      void* K, void* V, float* amax_kv, cudaStream_t st);
+cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int H, int d, int P, void* O,
+                                    cudaStream_t st);
+
+// Debug probes (codec checks against the oracle)
+cudaError_t launch_probe(int which, const void* in, void* out, int64_t n, cudaStream_t st);
+
+}  // namespace kvq

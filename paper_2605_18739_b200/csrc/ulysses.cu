@@ -1,0 +1,183 @@
+// ulysses.cu -- compute around the head-sharded (Ulysses) all-to-all of PAPER.md:556-564
+// (App. C): z^(p) in R^{L/P x H x d} -> R^{L x H/P x d} before attention, and back after.
+// The collective is NCCL (torch.distributed all_to_all_single over NVLink); these kernels pack
+// the per-destination head blocks (with the shard's amax(K), amax(V) piggybacked so every
+// owner takes alpha^FP32 over ALL heads -- readings Z2/Z18), unpack the received token blocks,
+// and interleave the returned O heads.  All copies are 128-bit and coalesced on both sides.
+#include "common.cuh"
+#include "internal.h"
+
+namespace kvq {
+namespace {
+
+constexpr int kMaxP = 64;
+
+struct PackParams {
+  const uint8_t* x[3];
+  uint8_t* send;
+  const uint32_t* partials;  // [2][kNumPartials] amax of the local K, V shard
+  int64_t seg_off[kMaxP];    // byte offset of destination p's segment
+  int h0[kMaxP + 1];         // head partition
+  uint8_t owner[256];        // head -> destination rank
+  int Ts, H, d, es, P;
+};
+
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
+  const int cpr = p.d * p.es / 16;  // 16-byte chunks per (t, h) row
+  const int64_t per_tensor = (int64_t)p.Ts * p.H * cpr;
+  const int64_t total = 3 * per_tensor;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int tsr = (int)(i / per_tensor);
+    const int64_t rem = i - tsr * per_tensor;
+    const int64_t row = rem / cpr;
+    const int c = (int)(rem - row * cpr);
+    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+    const int dst = p.owner[h];
+    const int Hp = p.h0[dst + 1] - p.h0[dst];
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.x[tsr] + row * p.d * p.es) + c);
+    uint8_t* o = p.send + p.seg_off[dst] + (((int64_t)tsr * p.Ts + t) * Hp + (h - p.h0[dst])) * p.d * p.es;
+    reinterpret_cast<uint4*>(o)[c] = v;
+  }
+  if (blockIdx.x == 0) {  // amax of the local shard -> every destination's trailer
+    __shared__ uint32_t red[2][8];
+    for (int tsr = 0; tsr < 2; ++tsr) {
+      uint32_t m = 0;
+      for (int k = threadIdx.x; k < kNumPartials; k += blockDim.x) m = max(m, p.partials[tsr * kNumPartials + k]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) red[tsr][threadIdx.x >> 5] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * kMaxP && (threadIdx.x >> 1) < p.P) {
+      const int tsr = threadIdx.x & 1, dst = threadIdx.x >> 1;
+      uint32_t m = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = max(m, red[tsr][w]);
+      const int Hp = p.h0[dst + 1] - p.h0[dst];
+      uint32_t* trailer = reinterpret_cast<uint32_t*>(p.send + p.seg_off[dst] + 3 * (int64_t)p.Ts * Hp * p.d * p.es);
+      trailer[tsr] = m;
+      if (tsr == 0) {
+        trailer[2] = 0;
+        trailer[3] = 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) unpack_qkv_kernel(const uint8_t* recv, int Ts, int Hr, int d, int es, int P,
+                                                         uint8_t* Q, uint8_t* K, uint8_t* V, float* amax_kv) {
+  const int64_t blk = (int64_t)Ts * Hr * d * es;  // bytes of one tensor block from one source
+  const int64_t seg = 3 * blk + 16;
+  const int64_t cpb = blk / 16;
+  const int64_t total = (int64_t)P * 3 * cpb;
+  uint8_t* outs[3] = {Q, K, V};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / cpb;  // (source, tensor) block
+    const int64_t c = i - b * cpb;
+    const int src = (int)(b / 3), tsr = (int)(b - (int64_t)src * 3);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(recv + src * seg + tsr * blk) + c);
+    reinterpret_cast<uint4*>(outs[tsr] + src * blk)[c] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2) {  // global amax = max over every source's shard amax
+    uint32_t m = 0;
+    for (int src = 0; src < P; ++src) m = max(m, reinterpret_cast<const uint32_t*>(recv + src * seg + 3 * blk)[threadIdx.x]);
+    amax_kv[threadIdx.x] = __uint_as_float(m);
+  }
+}
+
+struct UnpackOParams {
+  const uint8_t* recv;
+  uint8_t* out;
+  int64_t src_off[kMaxP];
+  int h0[kMaxP + 1];
+  uint8_t owner[256];
+  int Ts, H, d, es, P;
+};
+
+__global__ void __launch_bounds__(256) unpack_o_kernel(const __grid_constant__ UnpackOParams p) {
+  const int cpr = p.d * p.es / 16;
+  const int64_t total = (int64_t)p.Ts * p.H * cpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cpr;
+    const int c = (int)(i - row * cpr);
+    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+    const int src = p.owner[h];
+    const int Hp = p.h0[src + 1] - p.h0[src];
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.recv + p.src_off[src] +
+                                                         ((int64_t)t * Hp + (h - p.h0[src])) * p.d * p.es) + c);
+    reinterpret_cast<uint4*>(p.out + row * p.d * p.es)[c] = v;
+  }
+}
+
+int grid_for(int64_t work) {
+  int64_t g = (work + 255) / 256;
+  return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
+}
+
+void partition(int H, int P, int* h0, uint8_t* owner) {
+  const int base = H / P, rem = H % P;
+  h0[0] = 0;
+  for (int r = 0; r < P; ++r) h0[r + 1] = h0[r] + base + (r < rem ? 1 : 0);
+  for (int r = 0; r < P; ++r)
+    for (int h = h0[r]; h < h0[r + 1]; ++h) owner[h] = (uint8_t)r;
+}
+
+}  // namespace
+
+cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int dtype, int Ts, int H, int d, int P,
+                                uint8_t* send, uint32_t* scratch, cudaStream_t st) {
+  if (P > kMaxP || H > 256) return cudaErrorInvalidValue;
+  const int es = dtype == DT_FP32 ? 4 : 2;
+  cudaError_t e = launch_amax(K, V, dtype, (int64_t)Ts * H * d, scratch, reinterpret_cast<DevStatus*>(scratch + 2 * kNumPartials), st);
+  if (e != cudaSuccess) return e;
+  PackParams p{};
+  p.x[0] = (const uint8_t*)Q;
+  p.x[1] = (const uint8_t*)K;
+  p.x[2] = (const uint8_t*)V;
+  p.send = send;
+  p.partials = scratch;
+  partition(H, P, p.h0, p.owner);
+  int64_t off = 0;
+  for (int r = 0; r < P; ++r) {
+    p.seg_off[r] = off;
+    off += 3 * (int64_t)Ts * (p.h0[r + 1] - p.h0[r]) * d * es + 16;
+  }
+  p.Ts = Ts;
+  p.H = H;
+  p.d = d;
+  p.es = es;
+  p.P = P;
+  pack_kernel<<<grid_for(3 * (int64_t)Ts * H * d * es / 16), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ulysses_unpack_qkv(const uint8_t* recv, int dtype, int Ts, int Hr, int d, int P, void* Q, void* K,
+                                      void* V, float* amax_kv, cudaStream_t st) {
+  const int es = dtype == DT_FP32 ? 4 : 2;
+  unpack_qkv_kernel<<<grid_for((int64_t)P * 3 * Ts * Hr * d * es / 16), 256, 0, st>>>(
+      recv, Ts, Hr, d, es, P, (uint8_t*)Q, (uint8_t*)K, (uint8_t*)V, amax_kv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int H, int d, int P, void* O,
+                                    cudaStream_t st) {
+  if (P > kMaxP || H > 256) return cudaErrorInvalidValue;
+  const int es = dtype == DT_FP32 ? 4 : 2;
+  UnpackOParams p{};
+  p.recv = recv;
+  p.out = (uint8_t*)O;
+  partition(H, P, p.h0, p.owner);
+  int64_t off = 0;
+  for (int r = 0; r < P; ++r) {
+    p.src_off[r] = off;
+    off += (int64_t)Ts * (p.h0[r + 1] - p.h0[r]) * d * es;
+  }
+  p.Ts = Ts;
+  p.H = H;
+  p.d = d;
+  p.es = es;
+  p.P = P;
+  unpack_o_kernel<<<grid_for((int64_t)Ts * H * d * es / 16), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace kvq

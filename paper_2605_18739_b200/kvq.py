@@ -1,0 +1,339 @@
+"""Thin Python binding of libkvq.so (include/kvq.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; torch supplies device memory
+(the cache arena and all tensors), the current CUDA stream, and -- for the multi-GPU path --
+the process group.  There is no CPU fallback: if libkvq.so is missing or fails to load, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libkvq.so")
+_lib = None
+
+KVQ_BF16, KVQ_FP32, KVQ_FP16 = 0, 1, 2
+_STATUS = {0: "KVQ_OK", -1: "KVQ_EINVAL", -2: "KVQ_ESHAPE", -3: "KVQ_EDTYPE", -4: "KVQ_ENOCHUNK",
+           -5: "KVQ_ECAPACITY", -6: "KVQ_ENONFINITE", -7: "KVQ_ERANGE", -8: "KVQ_ECUDA", -9: "KVQ_ENCCL"}
+
+
+class KVQError(RuntimeError):
+    def __init__(self, code, where):
+        self.code = code
+        super().__init__(f"{where}: {_STATUS.get(code, code)} ({code})")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "num_layers", "num_heads", "head_dim", "tokens_per_frame", "frames_per_chunk", "sink_frames",
+        "window_frames", "max_chunk_slots", "scale_mode", "k_smoothing")]
+
+
+class _Mask(ctypes.Structure):
+    _fields_ = [("chunk_index", ctypes.c_int64), ("sink_frames", ctypes.c_int32),
+                ("window_frames", ctypes.c_int32), ("shot_start_frame", ctypes.c_int64),
+                ("shot_len_frames", ctypes.c_int64)]
+
+
+@dataclass
+class Mask:
+    """K_eff(t) = A_g U A_s U KV_[t-W,t) U {chunk t}, all in frames."""
+    chunk_index: int
+    sink_frames: int
+    window_frames: int
+    shot_start_frame: int = 0
+    shot_len_frames: int = 0
+
+    def _c(self):
+        return _Mask(self.chunk_index, self.sink_frames, self.window_frames, self.shot_start_frame,
+                     self.shot_len_frames)
+
+
+_P = ctypes.c_void_p
+_SIGS = {
+    "kvq_cache_bytes": (ctypes.c_size_t, [ctypes.POINTER(Config)]),
+    "kvq_cache_create": (ctypes.c_int, [ctypes.POINTER(Config), _P, ctypes.c_size_t, _P, ctypes.POINTER(_P)]),
+    "kvq_cache_destroy": (ctypes.c_int, [_P]),
+    "kvq_cache_reset": (ctypes.c_int, [_P, _P]),
+    "kvq_set_shot": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64]),
+    "kv_quantize_append": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P]),
+    "kv_quantize_append_amax": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P, _P]),
+    "chunk_attention": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int, ctypes.POINTER(_Mask), ctypes.c_float,
+                                       _P, ctypes.c_int, _P]),
+    "kv_dequantize": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P]),
+    "kv_export_chunk": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "kvq_resident_bytes": (ctypes.c_size_t, [_P]),
+    "kvq_resident_chunks": (ctypes.c_int32, [_P, ctypes.c_int32]),
+    "kv_dequantize_window": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(_Mask), _P, _P,
+                                            ctypes.POINTER(ctypes.c_int64), _P]),
+    "chunk_attention_bf16kv": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_float, _P, ctypes.c_int, _P]),
+    "kvq_get_status": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    "kvq_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "kvq_head_partition": (None, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_int32)]),
+    "kvq_ulysses_qkv_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 5 + [ctypes.c_int]),
+    "kvq_ulysses_pack_qkv": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, _P, _P, _P]),
+    "kvq_ulysses_unpack_qkv": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, _P, _P, _P, _P, _P]),
+    "kvq_ulysses_unpack_o": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, _P, _P]),
+    "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
+}
+
+
+def lib():
+    """Load libkvq.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"libkvq.so not built ({_LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code, where):
+    if code != 0:
+        raise KVQError(code, where)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dt(t: torch.Tensor):
+    if t.dtype == torch.bfloat16:
+        return KVQ_BF16
+    if t.dtype == torch.float32:
+        return KVQ_FP32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _ptr(t: torch.Tensor):
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _out_code(dtype):
+    return {torch.bfloat16: KVQ_BF16, torch.float32: KVQ_FP32}[dtype]
+
+
+class KVCache:
+    """Chunkwise NVFP4 KV cache of one rank over a torch-owned arena."""
+
+    def __init__(self, num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk,
+                 sink_frames=0, window_frames=None, max_chunk_slots=8, device=None):
+        L = lib()
+        window_frames = window_frames if window_frames is not None else max_chunk_slots * frames_per_chunk
+        self.cfg = Config(num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk, sink_frames,
+                          window_frames, max_chunk_slots, 0, 0)
+        nbytes = L.kvq_cache_bytes(ctypes.byref(self.cfg))
+        if nbytes == 0:
+            raise KVQError(-1, "kvq_cache_bytes (bad config)")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.arena = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.T_c = tokens_per_frame * frames_per_chunk
+        self.H, self.d = num_heads, head_dim
+        h = ctypes.c_void_p()
+        _check(L.kvq_cache_create(ctypes.byref(self.cfg), _ptr(self.arena), nbytes, _stream(), ctypes.byref(h)),
+               "kvq_cache_create")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.kvq_cache_destroy(self._h)
+            self._h = None
+
+    @property
+    def arena_bytes(self):
+        return self.arena.numel()
+
+    def reset(self):
+        _check(lib().kvq_cache_reset(self._h, _stream()), "kvq_cache_reset")
+
+    def set_shot(self, start_frame, len_frames):
+        _check(lib().kvq_set_shot(self._h, start_frame, len_frames), "kvq_set_shot")
+
+    def _shape_ok(self, t):
+        if tuple(t.shape) != (self.T_c, self.H, self.d):
+            raise ValueError(f"expected [{self.T_c}, {self.H}, {self.d}], got {tuple(t.shape)}")
+
+    def append(self, layer, chunk_index, K, V, amax_kv=None):
+        """kv_quantize_append (or kv_quantize_append_amax when amax_kv, a 2-float device tensor, is given)."""
+        self._shape_ok(K)
+        self._shape_ok(V)
+        if K.dtype != V.dtype:
+            raise TypeError("K and V dtypes differ")
+        if amax_kv is None:
+            _check(lib().kv_quantize_append(self._h, layer, chunk_index, _ptr(K), _ptr(V), _dt(K), _stream()),
+                   "kv_quantize_append")
+        else:
+            _check(lib().kv_quantize_append_amax(self._h, layer, chunk_index, _ptr(K), _ptr(V), _dt(K),
+                                                 _ptr(amax_kv), _stream()), "kv_quantize_append_amax")
+
+    def attention(self, layer, Q, mask: Mask, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None):
+        """chunk_attention: O = softmax(Q K^T * scale) V over K_eff(mask) with fused dequant."""
+        self._shape_ok(Q)
+        if out is None:
+            out = torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
+        m = mask._c()
+        _check(lib().chunk_attention(self._h, layer, _ptr(Q), _dt(Q), ctypes.byref(m), softmax_scale, _ptr(out),
+                                     _out_code(out.dtype), _stream()), "chunk_attention")
+        return out
+
+    def dequantize(self, layer, chunk_index, out_dtype=torch.float32):
+        K = torch.empty((self.T_c, self.H, self.d), dtype=out_dtype, device=self.device)
+        V = torch.empty_like(K)
+        _check(lib().kv_dequantize(self._h, layer, chunk_index, _ptr(K), _ptr(V), _out_code(out_dtype), _stream()),
+               "kv_dequantize")
+        return K, V
+
+    def export(self, layer, chunk_index):
+        rows = self.T_c * self.H
+        dev = self.device
+        out = {k: torch.empty((rows, self.d // 2), dtype=torch.uint8, device=dev) for k in ("codes_k", "codes_v")}
+        out.update({k: torch.empty((rows, self.d // 16), dtype=torch.uint8, device=dev) for k in ("scales_k", "scales_v")})
+        out.update({k: torch.empty(1, dtype=torch.float32, device=dev) for k in ("g_k", "g_v")})
+        _check(lib().kv_export_chunk(self._h, layer, chunk_index, _ptr(out["codes_k"]), _ptr(out["scales_k"]),
+                                     _ptr(out["g_k"]), _ptr(out["codes_v"]), _ptr(out["scales_v"]), _ptr(out["g_v"]),
+                                     _stream()), "kv_export_chunk")
+        return out
+
+    def n_keys(self, layer, mask: Mask):
+        n = ctypes.c_int64()
+        m = mask._c()
+        _check(lib().kv_dequantize_window(self._h, layer, ctypes.byref(m), None, None, ctypes.byref(n), _stream()),
+               "kv_dequantize_window")
+        return n.value
+
+    def dequantize_window(self, layer, mask: Mask, K_out=None, V_out=None):
+        """The paper's unfused reconstruction of K_eff into contiguous bf16 (bench comparison)."""
+        n = self.n_keys(layer, mask)
+        if K_out is None:
+            K_out = torch.empty((n, self.H, self.d), dtype=torch.bfloat16, device=self.device)
+            V_out = torch.empty_like(K_out)
+        nk = ctypes.c_int64()
+        m = mask._c()
+        _check(lib().kv_dequantize_window(self._h, layer, ctypes.byref(m), _ptr(K_out), _ptr(V_out),
+                                          ctypes.byref(nk), _stream()), "kv_dequantize_window")
+        return K_out, V_out
+
+    def resident_bytes(self):
+        return int(lib().kvq_resident_bytes(self._h))
+
+    def resident_chunks(self, layer):
+        return int(lib().kvq_resident_chunks(self._h, layer))
+
+    def status(self):
+        idx = ctypes.c_int64()
+        code = lib().kvq_get_status(self._h, _stream(), ctypes.byref(idx))
+        return code, idx.value
+
+
+def chunk_attention_bf16kv(Q, K, V, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None):
+    """Attention over caller-provided bf16 K/V [n_keys, H, d] (the A12 bf16-KV comparison mode)."""
+    Tq, H, d = Q.shape
+    if out is None:
+        out = torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
+    _check(lib().chunk_attention_bf16kv(_ptr(Q), _ptr(K), _ptr(V), Tq, K.shape[0], H, d, softmax_scale, _ptr(out),
+                                        _out_code(out.dtype), _stream()), "chunk_attention_bf16kv")
+    return out
+
+
+def probe(which, x, n):
+    """kvq_debug_probe: run one hardware NVFP4 conversion over a device buffer (codec checks)."""
+    out_shape = {0: (2 * n,), 1: (n,), 2: (2 * n,), 3: (n,)}[which]
+    out_dtype = {0: torch.uint8, 1: torch.uint8, 2: torch.float32, 3: torch.float32}[which]
+    out = torch.empty(out_shape, dtype=out_dtype, device=x.device)
+    _check(lib().kvq_debug_probe(which, _ptr(x), _ptr(out), n, _stream()), "kvq_debug_probe")
+    return out
+
+
+def head_partition(H, P, rank):
+    h0, h1 = ctypes.c_int32(), ctypes.c_int32()
+    lib().kvq_head_partition(H, P, rank, ctypes.byref(h0), ctypes.byref(h1))
+    return h0.value, h1.value
+
+
+def ulysses_qkv_bytes(Ts, H, d, P, dst, dtype=torch.bfloat16):
+    return int(lib().kvq_ulysses_qkv_bytes(Ts, H, d, P, dst, _out_code(dtype)))
+
+
+class Ulysses:
+    """Head-sharded chunk step of one rank (App. C; App. D).
+
+    pack (kernel) -> all_to_all_single (NCCL, torch.distributed) -> unpack + global amax (kernel)
+    -> kv_quantize_append_amax + chunk_attention on the local heads (kernels) -> all_to_all_single
+    of O (NCCL) -> head interleave (kernel).
+    """
+
+    def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.cache, self.H, self.d, self.T_c = cache, H, d, T_c
+        self.rank, self.P = rank, world
+        if T_c % world:
+            raise ValueError("T_c must be divisible by the SP degree")
+        self.Ts = T_c // world
+        self.h0, self.h1 = head_partition(H, world, rank)
+        self.Hr = self.h1 - self.h0
+        if cache.H != self.Hr:
+            raise ValueError("cache must hold exactly this rank's heads")
+        dev = cache.device
+        es = 2 if dtype == torch.bfloat16 else 4
+        self.dtype = dtype
+        self.send_sizes = [ulysses_qkv_bytes(self.Ts, H, d, world, p, dtype) for p in range(world)]
+        self.recv_seg = ulysses_qkv_bytes(self.Ts, H, d, world, rank, dtype)
+        self.send = torch.empty(sum(self.send_sizes), dtype=torch.uint8, device=dev)
+        self.recv = torch.empty(self.recv_seg * world, dtype=torch.uint8, device=dev)
+        self.scratch = torch.empty(8192, dtype=torch.uint8, device=dev)
+        self.Q = torch.empty((T_c, self.Hr, d), dtype=dtype, device=dev)
+        self.K = torch.empty_like(self.Q)
+        self.V = torch.empty_like(self.Q)
+        self.amax = torch.empty(2, dtype=torch.float32, device=dev)
+        self.O_local = torch.empty((T_c, self.Hr, d), dtype=torch.bfloat16, device=dev)
+        self.o_recv_sizes = [self.Ts * (head_partition(H, world, p)[1] - head_partition(H, world, p)[0]) * d * 2
+                             for p in range(world)]
+        self.o_recv = torch.empty(sum(self.o_recv_sizes), dtype=torch.uint8, device=dev)
+        self.es = es
+
+    def step(self, layer, chunk_index, Q, K, V, mask: Mask, out=None):
+        """One layer of one chunk: Q, K, V are this rank's sequence shards [T_c/P, H, d]."""
+        L, st = lib(), _stream()
+        dt = _dt(Q)
+        _check(L.kvq_ulysses_pack_qkv(_ptr(Q), _ptr(K), _ptr(V), dt, self.Ts, self.H, self.d, self.P,
+                                      _ptr(self.send), _ptr(self.scratch), st), "kvq_ulysses_pack_qkv")
+        self.dist.all_to_all_single(self.recv, self.send, output_split_sizes=[self.recv_seg] * self.P,
+                                    input_split_sizes=self.send_sizes, group=self.group)
+        _check(L.kvq_ulysses_unpack_qkv(_ptr(self.recv), dt, self.Ts, self.Hr, self.d, self.P, _ptr(self.Q),
+                                        _ptr(self.K), _ptr(self.V), _ptr(self.amax), st), "kvq_ulysses_unpack_qkv")
+        self.cache.append(layer, chunk_index, self.K, self.V, amax_kv=self.amax)
+        self.cache.attention(layer, self.Q, mask, out=self.O_local)
+        o_send = self.O_local.view(torch.uint8).reshape(-1)
+        self.dist.all_to_all_single(self.o_recv, o_send, output_split_sizes=self.o_recv_sizes,
+                                    input_split_sizes=[o_send.numel() // self.P] * self.P, group=self.group)
+        if out is None:
+            out = torch.empty((self.Ts, self.H, self.d), dtype=torch.bfloat16, device=Q.device)
+        _check(L.kvq_ulysses_unpack_o(_ptr(self.o_recv), KVQ_BF16, self.Ts, self.H, self.d, self.P, _ptr(out), st),
+               "kvq_ulysses_unpack_o")
+        return out
+
+
+def softmax_scale_default(d):
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,305 @@
+"""CUDA path vs the float64 oracle, through the C ABI (-m gpu).
+
+Bar (BASELINE.json north_star): codes, scales and tensor scales bit-exact; attention in the
+fp32-out parity mode within max-abs 2e-3 and rel-L2 1e-3; bf16 output within 1 bf16 ulp of
+RN_bf16(oracle) (reading Z17).  Inputs come from paper_2605_18739_b200.synth (seeded; the
+oracle and the GPU consume the same bytes).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import nvfp4
+from oracle.cache import OracleKVCache
+from oracle.keyset import key_token_ranges
+from paper_2605_18739_b200 import kvq, synth
+
+from gpu_util import assert_chunk_bytes_equal, check_bf16_out, check_fp32_out
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+# --------------------------------------------------------------------------- codec probes
+def test_probe_e2m1_encode_matches_oracle():
+    _gpu()
+    base = np.concatenate([np.linspace(-8, 8, 400001), np.arange(-7, 7.01, 0.25), [-0.0, 0.0, -1e-30, 1e30, -1e30,
+                                                                                   2.0 ** -149, -(2.0 ** -149)]])
+    # all fp32 neighbours of every midpoint
+    mids = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0])
+    nb = np.concatenate([np.nextafter(mids.astype(np.float32), np.float32(0)), np.nextafter(mids.astype(np.float32), np.float32(9))])
+    x = np.concatenate([base, nb, -nb]).astype(np.float32)
+    if x.size % 2:
+        x = np.append(x, np.float32(0))
+    got = kvq.probe(0, torch.from_numpy(x).to(DEV), x.size // 2).cpu().numpy()
+    want = nvfp4.e2m1_encode(x.astype(np.float64))
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+
+
+def test_probe_e4m3_encode_matches_oracle():
+    _gpu()
+    v = nvfp4.e4m3_decode(np.arange(0x7F))
+    mids = (v[1:] + v[:-1]) / 2
+    x = np.concatenate([np.linspace(0, 464, 300001), np.exp2(np.linspace(-14, 8.9, 100001)), v, mids,
+                        np.nextafter(mids.astype(np.float32), np.float32(0)),
+                        np.nextafter(mids.astype(np.float32), np.float32(1000))]).astype(np.float32)
+    got = kvq.probe(1, torch.from_numpy(x).to(DEV), x.size).cpu().numpy()
+    want = nvfp4.e4m3_encode_nonneg(x.astype(np.float64))
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+
+
+def test_probe_decoders_exhaustive():
+    _gpu()
+    b = torch.arange(256, dtype=torch.uint8, device=DEV)
+    e2 = kvq.probe(2, b, 256).cpu().numpy().reshape(256, 2)
+    ref = np.stack([nvfp4.e2m1_decode(np.arange(256) & 0xF), nvfp4.e2m1_decode(np.arange(256) >> 4)], 1)
+    assert np.array_equal(e2, ref)   # low nibble first (reading Z8)
+    e4 = kvq.probe(3, b, 256).cpu().numpy()
+    ref4 = nvfp4.e4m3_decode(np.arange(256))
+    ok = ~np.isnan(ref4)
+    assert np.array_equal(e4[ok], ref4[ok])
+
+
+# --------------------------------------------------------------------------- quantize / append
+def _cache(H, d, tpf, fc, sink=0, window=None, slots=8, layers=1):
+    return kvq.KVCache(layers, H, d, tpf, fc, sink_frames=sink, window_frames=window or slots * fc,
+                       max_chunk_slots=slots, device=DEV)
+
+
+def test_quantize_tiny_bitexact():
+    _gpu()
+    T, H, d = 64, 2, 64
+    c = _cache(H, d, 64, 1)
+    for ch in range(3):
+        _, k, v = synth.make_qkv(T, H, d, "fp32", 0, ch)
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        assert_chunk_bytes_equal(c.export(0, ch), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
+
+
+@pytest.mark.parametrize("variant,scale", [("iid", 1.0), ("outlier", 1.0), ("iid", 0.37), ("iid", 45.0),
+                                           ("iid", 0.01)])
+def test_quantize_wan_shape_bitexact(variant, scale):
+    _gpu()
+    T, H, d = 4680, 12, 128
+    c = _cache(H, d, 1560, 3)
+    _, k, v = synth.make_qkv(T, H, d, "bf16", 3, 7, variant=variant)
+    if scale != 1.0:
+        k = synth.Tensor(k.f64 * scale, "bf16")
+        v = synth.Tensor(v.f64 * scale, "bf16")
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
+
+
+def test_quantize_edge_blocks_bitexact():
+    # zero tensor (g = 1), zero blocks, underflow-promoted scales, -0.0, ragged T_c (not a multiple of 128)
+    _gpu()
+    T, H, d = 40, 3, 128
+    c = _cache(H, d, 40, 1)
+    x = synth.make_tensor((T, H, d), "bf16", seed=5).f64
+    x[:, :, 16:32] = 0.0
+    x[3, 1, 32:48] = x[3, 1, 32:48] * 1e-6
+    x[4, 0, 0] = -0.0
+    x[7, 2, 5] = 2688.0 * 4
+    x = synth.Tensor(x, "bf16").f64
+    z = np.zeros((T, H, d))
+    c.append(0, 0, synth.Tensor(x, "bf16").torch(DEV), synth.Tensor(z, "bf16").torch(DEV))
+    assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(x), nvfp4.quantize_kv_chunk(z))
+
+
+def test_dequantize_bitexact():
+    _gpu()
+    T, H, d = 120, 4, 128
+    c = _cache(H, d, 40, 3)
+    _, k, v = synth.make_qkv(T, H, d, "bf16", 0, 0)
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    K32, V32 = c.dequantize(0, 0, torch.float32)
+    refK = nvfp4.dequantize_kv_chunk(nvfp4.quantize_kv_chunk(k.f64), T, H, d)
+    refV = nvfp4.dequantize_kv_chunk(nvfp4.quantize_kv_chunk(v.f64), T, H, d)
+    assert np.array_equal(K32.cpu().numpy(), refK.astype(np.float32))
+    assert np.array_equal(V32.cpu().numpy(), refV.astype(np.float32))
+    Kb, _ = c.dequantize(0, 0, torch.bfloat16)
+    assert torch.equal(Kb.cpu(), torch.from_numpy(refK.astype(np.float32)).to(torch.bfloat16))
+
+
+def test_nonfinite_reported():
+    _gpu()
+    T, H, d = 64, 2, 64
+    c = _cache(H, d, 64, 1)
+    _, k, v = synth.make_qkv(T, H, d, "fp32", 0, 0)
+    kk = k.torch(DEV)
+    kk.view(-1)[1234] = float("inf")
+    c.append(0, 0, kk, v.torch(DEV))
+    code, idx = c.status()
+    assert code == -6 and idx == 1234
+    assert c.status() == (0, -1)
+
+
+# --------------------------------------------------------------------------- attention
+def _run_chunks(T, H, d, tpf, fc, n_chunks, dtype, sink, window, slots, variant="iid", layers=1):
+    c = _cache(H, d, tpf, fc, sink, window, slots, layers)
+    o = OracleKVCache(layers, H, d, tpf, fc)
+    data = []
+    for ch in range(n_chunks):
+        q, k, v = synth.make_qkv(T, H, d, dtype, 0, ch, variant=variant)
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        o.append(0, ch, k.f64, v.f64)
+        data.append(q)
+    return c, o, data
+
+
+def test_attention_tiny_full_window():
+    _gpu()
+    T, H, d = 64, 2, 64
+    c, o, qs = _run_chunks(T, H, d, 64, 1, 3, "fp32", 0, 1 << 20, 8)
+    for variant in ("iid",):
+        for ch in range(3):
+            m = kvq.Mask(ch, 0, 1 << 20)
+            O32 = c.attention(0, qs[ch].torch(DEV), m, torch.float32).cpu().numpy()
+            ref = o.attend(0, ch, qs[ch].f64, 0, 1 << 20)
+            check_fp32_out(O32, ref)
+            Ob = c.attention(0, qs[ch].torch(DEV), m, torch.bfloat16).float().cpu().numpy()
+            check_bf16_out(Ob, ref, O32)
+
+
+@pytest.mark.parametrize("variant", ["iid", "peaked", "outlier"])
+def test_attention_tiny_variants(variant):
+    _gpu()
+    T, H, d = 64, 2, 64
+    c, o, qs = _run_chunks(T, H, d, 64, 1, 3, "fp32", 0, 1 << 20, 8, variant=variant)
+    O32 = c.attention(0, qs[2].torch(DEV), kvq.Mask(2, 0, 1 << 20), torch.float32).cpu().numpy()
+    check_fp32_out(O32, o.attend(0, 2, qs[2].f64, 0, 1 << 20))
+
+
+def test_attention_sink_window_ragged_d128():
+    # W30-like mask at small scale: T_c = 120 (ragged vs 128-key tiles), sink 3 frames, window 9 frames
+    _gpu()
+    T, H, d, tpf, fc = 120, 3, 128, 40, 3
+    sink, window = 3, 9
+    c = _cache(H, d, tpf, fc, sink, window, 8)
+    o = OracleKVCache(1, H, d, tpf, fc)
+    for ch in range(9):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch)
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        o.append(0, ch, k.f64, v.f64)
+        m = kvq.Mask(ch, sink, window)
+        O32 = c.attention(0, q.torch(DEV), m, torch.float32).cpu().numpy()
+        check_fp32_out(O32, o.attend(0, ch, q.f64, sink, window))
+        assert c.resident_chunks(0) <= 8
+    # a mask reaching an evicted chunk is refused
+    with pytest.raises(kvq.KVQError) as e:
+        c.attention(0, q.torch(DEV), kvq.Mask(8, 0, 27), torch.float32)
+    assert e.value.code == -4
+
+
+def test_attention_shot_sink_and_partial_frames():
+    # sink of 1 frame (mid-chunk boundary), a shot sink, window not a multiple of the chunk
+    _gpu()
+    T, H, d, tpf, fc = 96, 2, 64, 32, 3
+    c = _cache(H, d, tpf, fc, sink=1, window=7, slots=8)
+    o = OracleKVCache(1, H, d, tpf, fc)
+    c.set_shot(12, 4)
+    for ch in range(10):
+        q, k, v = synth.make_qkv(T, H, d, "fp32", 0, ch)
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        o.append(0, ch, k.f64, v.f64)
+        if ch >= 4:
+            m = kvq.Mask(ch, 1, 7, 12, 4)
+            O32 = c.attention(0, q.torch(DEV), m, torch.float32).cpu().numpy()
+            check_fp32_out(O32, o.attend(0, ch, q.f64, 1, 7, 12, 4))
+
+
+def test_overwrite_newest_chunk():
+    # a denoising step re-writes the in-progress chunk (chunk_index == newest)
+    _gpu()
+    T, H, d = 64, 2, 64
+    c = _cache(H, d, 64, 1)
+    _, k, v = synth.make_qkv(T, H, d, "fp32", 0, 0)
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    _, k2, v2 = synth.make_qkv(T, H, d, "fp32", 0, 5)
+    c.append(0, 0, k2.torch(DEV), v2.torch(DEV))
+    assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(k2.f64), nvfp4.quantize_kv_chunk(v2.f64))
+    with pytest.raises(kvq.KVQError):
+        c.append(0, 2, k.torch(DEV), v.torch(DEV))
+
+
+@pytest.fixture(scope="module")
+def wan_layer():
+    """Wan2.1-1.3B-shaped single layer: 12 heads x 128, T_c = 3 x 1560, window 21 frames (7 chunks)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, H, d, tpf, fc = 4680, 12, 128, 1560, 3
+    c = _cache(H, d, tpf, fc, sink=3, window=21, slots=8)
+    o = OracleKVCache(1, H, d, tpf, fc)
+    q = None
+    for ch in range(7):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch)
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        o.append(0, ch, k.f64, v.f64)
+    return c, o, q
+
+
+ROWS = np.array([0, 1, 63, 64, 127, 128, 129, 1000, 2047, 2048, 3333, 4095, 4096, 4500, 4607, 4608, 4609, 4679])
+
+
+def test_attention_wan_layer_sampled(wan_layer):
+    c, o, q = wan_layer
+    m = kvq.Mask(6, 3, 21)
+    assert c.n_keys(0, m) == 32760
+    O32 = c.attention(0, q.torch(DEV), m, torch.float32).cpu().numpy()
+    ref = o.attend(0, 6, q.f64, 3, 21, rows=ROWS)
+    check_fp32_out(O32[ROWS], ref)
+    Ob = c.attention(0, q.torch(DEV), m, torch.bfloat16).float().cpu().numpy()
+    check_bf16_out(Ob[ROWS], ref, O32[ROWS])
+
+
+def test_attention_wan_layer_properties(wan_layer):
+    # at full size: every output row is a convex combination of V^ rows -> within [min V^, max V^]
+    c, o, q = wan_layer
+    O = c.attention(0, q.torch(DEV), kvq.Mask(6, 3, 21), torch.float32)
+    assert torch.isfinite(O).all()
+    Kw, Vw = c.dequantize_window(0, kvq.Mask(6, 3, 21))
+    vmin = Vw.float().amin(0)
+    vmax = Vw.float().amax(0)
+    assert bool((O >= vmin - 1e-3).all()) and bool((O <= vmax + 1e-3).all())
+
+
+def test_dequantize_window_matches_oracle(wan_layer):
+    c, o, q = wan_layer
+    Kw, Vw = c.dequantize_window(0, kvq.Mask(6, 3, 21))
+    Kr, Vr = o.keys(0, 6, 3, 21)
+    idx = np.arange(0, Kr.shape[0], 997)
+    assert torch.equal(Kw[idx].cpu(), torch.from_numpy(Kr[idx].astype(np.float32)).to(torch.bfloat16))
+    assert torch.equal(Vw[idx].cpu(), torch.from_numpy(Vr[idx].astype(np.float32)).to(torch.bfloat16))
+
+
+def test_bf16kv_mode_against_oracle():
+    # A12 comparison mode: bf16 K/V, bf16 P (documented looser numerics: rel-L2 <= 4e-3)
+    _gpu()
+    Tq, H, d, N = 300, 2, 128, 700
+    Q = synth.make_tensor((Tq, H, d), "bf16", seed=1)
+    K = synth.make_tensor((N, H, d), "bf16", seed=2)
+    V = synth.make_tensor((N, H, d), "bf16", seed=3)
+    O = kvq.chunk_attention_bf16kv(Q.torch(DEV), K.torch(DEV), V.torch(DEV), torch.float32).cpu().numpy()
+    from oracle.attention import attention
+    ref = attention(Q.f64, K.f64, V.f64)
+    err = np.abs(O - ref).max()
+    rel = np.linalg.norm(O - ref) / np.linalg.norm(ref)
+    assert err < 1e-2 and rel < 4e-3, (err, rel)
+
+
+def test_resident_footprint_ratio():
+    # NVFP4 K+V payload vs bf16 -> 32/9 up to the two fp32 tensor scales per chunk
+    _gpu()
+    T, H, d = 4680, 12, 128
+    c = _cache(H, d, 1560, 3)
+    _, k, v = synth.make_qkv(T, H, d, "bf16", 0, 0)
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    nv = c.resident_bytes()
+    assert nv == nvfp4.storage_bytes(T, H, d)
+    assert abs((4 * T * H * d) / (nv - 8) - 32 / 9) < 1e-12
