@@ -4,21 +4,27 @@
 // Computes chunk_attention (include/kvq.h): for the current chunk's queries and head h,
 //   O = softmax(Q K^T * scale) V over the effective key set K_eff(t)
 // (§4.2; the cache of PAPER.md:134-146 §3.2), where K^, V^ are the
-// NVFP4 values of Eq. 2.  Dequantization is fused (the paper's separate
-// "parallel dequantization kernel", is prior art replaced here).
+// NVFP4 values of Eq. 2.  Dequantization is fused: the paper's separate
+// "parallel dequantization kernel" is prior art that this kernel replaces.
 //
 // Numerics: K^' = dec(code) * dec(s) and V^' likewise are EXACT in fp16, so the
 // tensor cores see the exact quantized lattice; the FP32 tensor scales g_K, g_V are applied in
-// fp32 outside the MMA (g_K in the exponent scale, g_V folded into the running O rescale).
-// Q is rounded once to fp16, P is fp16, accumulation is fp32 in TMEM.
+// fp32 outside the MMA (g_K in the exponent scale, g_V folded into the O rescale factor).
+// Q is rounded once to fp16, P is fp16, accumulation is fp32 in TMEM, the running max is exact
+// (no lazy threshold), l is summed in fp32 from the fp16-rounded P.
 //
-// Structure (v0 -- correctness first, one CTA per (128-query tile, head), 4 warps, thread i owns
-// query row i = TMEM lane i):
-//   per 128-key tile: all threads dequantize K/V rows into 128B-swizzled smem (UMMA K-major
-//   layout; V's identical bytes are read through an MN-major descriptor) -> one thread issues
-//   S = Q K^T (tcgen05.mma kind::f16, M=128 N=128, accumulator in TMEM) -> every thread loads
-//   its S row from TMEM, online softmax, writes fp16 P back into TMEM over S -> one thread
-//   issues O += P V (A operand from TMEM) -> next tile.  Epilogue O * g_V / l.
+// Structure: one CTA = one head x two 128-query tiles (256 rows share every dequantized KV
+// tile), warp-specialized, 13 warps:
+//   warps 0-3   softmax WG0  (query tile 0; thread i owns row i = TMEM lane i)
+//   warps 4-7   softmax WG1  (query tile 1)
+//   warps 8-11  dequant WG   (packed codes + E4M3 scales from L2 -> fp16 K^', V^' rows in
+//                             128B-swizzled smem, double buffered)
+//   warp 12     MMA issuer   (one thread issues tcgen05.mma; TMEM allocator)
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_i (fp16) overwrites
+// the first 64 columns of S_i.  Ping-pong: while WG0 exponentiates S0(j) the tensor core runs
+// QK1(j); while WG1 works on S1(j) it runs PV0(j) and QK0(j+1).  All hand-offs are mbarriers
+// (tcgen05.commit for MMA completion); MMAs execute in issue order, so the commit that signals
+// S_i(j+1) also guarantees PV_i(j) finished (O_i stable for the rescale, P_i(j) consumed).
 #include <cmath>
 
 #include "common.cuh"
@@ -27,60 +33,33 @@
 namespace kvq {
 namespace {
 
-constexpr int kBM = 128;
+constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant, MMA (+3 idle warps)
+// Register budget per SM sub-partition (16K regs = 4 warps x 128 at launch), rebalanced with
+// setmaxnreg: softmax 176 + 176, dequant 80, MMA warpgroup 80 (sum 512 per thread slot).
+constexpr int kRegSoftmax = 176, kRegDequant = 80, kRegMma = 80;
+
+template <int N>
+KVQ_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+KVQ_DEV void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
 template <int D>
-struct AttnSmem {
-  static constexpr int kTile = 128 * D * 2;  // 128 rows x D 16-bit values
-  static constexpr int kQ = 0;
-  static constexpr int kK = kTile;
-  static constexpr int kV = 2 * kTile;
-  static constexpr int kBar = 3 * kTile;
-  static constexpr int kBytes = kBar + 64 + 1024;  // + barriers + alignment slack
+struct WsSmem {
+  static constexpr int kTile = 128 * D * 2;
+  static constexpr int kQ0 = 0;
+  static constexpr int kQ1 = kTile;
+  static constexpr int kK0 = 2 * kTile;
+  static constexpr int kK1 = 3 * kTile;
+  static constexpr int kV0 = 4 * kTile;
+  static constexpr int kV1 = 5 * kTile;
+  static constexpr int kBar = 6 * kTile;
+  // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
+  static constexpr int kBytes = kBar + 16 * 8 + 16 + 1024;
 };
 
 // address of 16-byte chunk c (8 consecutive elements along d) of row r in a 128-row tile
-KVQ_DEV uint32_t chunk_addr(uint32_t base, int r, int c) { return base + (uint32_t)(c >> 3) * 16384u + sw128_off(r, c & 7); }
-
-// Dequantize one cache row (D values) into the tile: K^' = dec(code) * dec(s), exact in fp16.
-template <int D>
-KVQ_DEV void dequant_row_to_smem(uint32_t base, int r, const uint8_t* crow, const uint8_t* srow) {
-  uint32_t cw[D / 8];
-#pragma unroll
-  for (int k = 0; k < D / 32; ++k) {
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(crow) + k);
-    cw[4 * k] = v.x; cw[4 * k + 1] = v.y; cw[4 * k + 2] = v.z; cw[4 * k + 3] = v.w;
-  }
-  uint32_t sw[D / 64 > 0 ? D / 64 : 1];
-  if (D == 128) {
-    uint2 s2 = __ldg(reinterpret_cast<const uint2*>(srow));
-    sw[0] = s2.x; sw[1] = s2.y;
-  } else {
-    sw[0] = __ldg(reinterpret_cast<const uint32_t*>(srow));
-  }
-#pragma unroll
-  for (int j = 0; j < D / 16; ++j) {
-    const uint32_t sb = (sw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-    const uint32_t s2 = f16x2_from_e4m3x2(sb | (sb << 8));
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t w = cw[2 * j + half];
-      uint32_t o[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) o[b] = hmul2_u32(f16x2_from_e2m1x2((w >> (8 * b)) & 0xFF), s2);
-      st_shared_v4(chunk_addr(base, r, 2 * j + half), o[0], o[1], o[2], o[3]);
-    }
-  }
-}
-
-// Copy one bf16 row (D values) into the tile (bf16-KV mode), zeros when !valid.
-template <int D>
-KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool valid) {
-#pragma unroll
-  for (int c = 0; c < D / 8; ++c) {
-    uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(row) + c) : make_uint4(0, 0, 0, 0);
-    st_shared_v4(chunk_addr(base, r, c), v.x, v.y, v.z, v.w);
-  }
+KVQ_DEV uint32_t chunk_addr(uint32_t base, int r, int c) {
+  return base + (uint32_t)(c >> 3) * 16384u + sw128_off(r, c & 7);
 }
 
 KVQ_DEV uint32_t pack_half2(float a, float b) {
@@ -92,7 +71,57 @@ KVQ_DEV uint32_t pack_bf162(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Q row -> fp16 (or bf16 in bf16-KV mode) into the tile
+// Packed cache row (D values): D/2 code bytes + D/16 scale bytes, loaded to registers.
+template <int D>
+struct PackedRow {
+  uint4 c[D / 32];
+  uint32_t s[D / 64 > 0 ? D / 64 : 1];
+};
+
+template <int D>
+KVQ_DEV void load_packed_row(PackedRow<D>& r, const uint8_t* crow, const uint8_t* srow) {
+#pragma unroll
+  for (int k = 0; k < D / 32; ++k) r.c[k] = __ldg(reinterpret_cast<const uint4*>(crow) + k);
+  if (D == 128) {
+    uint2 s2 = __ldg(reinterpret_cast<const uint2*>(srow));
+    r.s[0] = s2.x;
+    r.s[1] = s2.y;
+  } else {
+    r.s[0] = __ldg(reinterpret_cast<const uint32_t*>(srow));
+  }
+}
+
+// K^' = dec(code) * dec(s) in fp16 (exact), written as one 128B-swizzled tile row.
+template <int D>
+KVQ_DEV void store_dequant_row(uint32_t base, int r, const PackedRow<D>& pr) {
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) {
+    const uint32_t sb = (pr.s[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t s2 = f16x2_from_e4m3x2(sb | (sb << 8));
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int wi = 2 * j + half;  // 32-bit code word index
+      const uint4 q = pr.c[wi >> 2];
+      const uint32_t w = (wi & 3) == 0 ? q.x : (wi & 3) == 1 ? q.y : (wi & 3) == 2 ? q.z : q.w;
+      uint32_t o[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) o[b] = hmul2_u32(f16x2_from_e2m1x2((w >> (8 * b)) & 0xFF), s2);
+      st_shared_v4(chunk_addr(base, r, wi), o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// bf16 row (bf16-KV comparison mode): copy D values, zeros when !valid
+template <int D>
+KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool valid) {
+#pragma unroll
+  for (int c = 0; c < D / 8; ++c) {
+    uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(row) + c) : make_uint4(0, 0, 0, 0);
+    st_shared_v4(chunk_addr(base, r, c), v.x, v.y, v.z, v.w);
+  }
+}
+
+// Q row -> fp16 (bf16 in bf16-KV mode) into a tile row
 template <int D, bool MMA_BF16>
 KVQ_DEV void load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_t row_index, bool valid) {
 #pragma unroll
@@ -107,143 +136,173 @@ KVQ_DEV void load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_
         } else {
           uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            f[2 * k] = __uint_as_float(w[k] << 16);
-            f[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) o[k] = pack_half2(f[2 * k], f[2 * k + 1]);
+          for (int k = 0; k < 4; ++k) o[k] = pack_half2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
         }
       } else {
         const float4* src = reinterpret_cast<const float4*>((const float*)Q + row_index * D) + 2 * c;
         float4 a = __ldg(src), b = __ldg(src + 1);
         f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
+        for (int k = 0; k < 4; ++k)
+          o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
       }
     }
     st_shared_v4(chunk_addr(base, r, c), o[0], o[1], o[2], o[3]);
   }
 }
 
+// Tile iteration over the key segments: tile = 128 slot-aligned rows, valid rows [lo, hi).
+struct TileIter {
+  int seg, t0;
+};
+KVQ_DEV bool tile_first(const AttnParams& p, TileIter& it) {
+  it.seg = 0;
+  if (p.nseg == 0) return false;
+  it.t0 = p.seg[0].begin & ~127;
+  return true;
+}
+KVQ_DEV bool tile_next(const AttnParams& p, TileIter& it) {
+  it.t0 += 128;
+  if (it.t0 < p.seg[it.seg].end) return true;
+  if (++it.seg >= p.nseg) return false;
+  it.t0 = p.seg[it.seg].begin & ~127;
+  return true;
+}
+KVQ_DEV int count_tiles(const AttnParams& p) {
+  int n = 0;
+  for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 127) >> 7) - (p.seg[s].begin >> 7);
+  return n;
+}
+
 template <int D, bool NVFP4, bool MMA_BF16>
-__global__ void __launch_bounds__(128, 1) attn_kernel(const __grid_constant__ AttnParams p) {
-  using SM = AttnSmem<D>;
+__global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
+  using SM = WsSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_u32(smem + SM::kQ), sK = smem_u32(smem + SM::kK), sV = smem_u32(smem + SM::kV);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::kBar);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + SM::kBar + 16);
+  // tile bases: Q_i = sbase + i*T, K_b = sbase + (2+b)*T, V_b = sbase + (4+b)*T
+  const uint32_t sbase = smem_u32(smem);
+  constexpr uint32_t kT = SM::kTile;
+#define SQ(i) (sbase + (uint32_t)(i) * kT)
+#define SK(b) (sbase + (2u + (uint32_t)(b)) * kT)
+#define SV(b) (sbase + (4u + (uint32_t)(b)) * kT)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+  uint64_t* kfull = bars + 0;   // [2]
+  uint64_t* vfull = bars + 2;   // [2]
+  uint64_t* kempty = bars + 4;  // [2]
+  uint64_t* vempty = bars + 6;  // [2]
+  uint64_t* sfull = bars + 8;   // [2] per query tile
+  uint64_t* pfull = bars + 10;  // [2]
+  uint64_t* ofull = bars + 12;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int h = blockIdx.y;
-  const int q0 = blockIdx.x * kBM;
+  const int q0 = blockIdx.x * 256;
   const int H = p.H;
+  const int ntiles = count_tiles(p);
 
-  if (warp == 0) tmem_alloc(tslot, 256);
+  if (warp == 12) tmem_alloc(tslot, 512);
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(kfull + b, 128);
+      mbar_init(vfull + b, 128);
+      mbar_init(kempty + b, 1);
+      mbar_init(vempty + b, 1);
+      mbar_init(sfull + b, 1);
+      mbar_init(pfull + b, 128);
+      mbar_init(ofull + b, 1);
+    }
     fence_mbar_init();
   }
-  {
+  // Q tiles (256 rows): threads 0..255 each load one row
+  if (tid < 256) {
     const int t = q0 + tid;
-    load_q_row<D, MMA_BF16>(sQ, tid, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+    load_q_row<D, MMA_BF16>(SQ(tid >> 7), tid & 127, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
   }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 128;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  constexpr uint32_t kIdS = umma_idesc_f16(128, 128, MMA_BF16 ? 1 : 0, 0, 0);
-  constexpr uint32_t kIdO = umma_idesc_f16(128, D, MMA_BF16 ? 1 : 0, 0, 1);
 
-  float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
-  uint32_t phase = 0;
-  int ntile = 0;
-
-  for (int sgi = 0; sgi < p.nseg; ++sgi) {
-    const AttnSeg sg = p.seg[sgi];
-    for (int t0 = sg.begin & ~127; t0 < sg.end; t0 += 128) {
-      const int lo = max(sg.begin - t0, 0), hi = min(sg.end - t0, 128);
+  if (warp < 8) {
+    // ================================================================ softmax WG (tile qi)
+    reg_alloc<kRegSoftmax>();
+    const int qi = warp >> 2;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + 128 * qi + lane_off;
+    const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
+    float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
+    TileIter it;
+    bool more = tile_first(p, it);
+    for (int j = 0; more; ++j, more = tile_next(p, it)) {
+      const AttnSeg& sg = p.seg[it.seg];
+      const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, 128);
       float gk = 1.0f, gv = 1.0f;
-      // ---- K / V tile -> swizzled smem (thread tid owns key row tid of the tile)
       if (NVFP4) {
-        const int64_t row = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + t0 + tid;
-        dequant_row_to_smem<D>(sK, tid, p.codes_k + row * (D / 2), p.scales_k + row * (D / 16));
-        dequant_row_to_smem<D>(sV, tid, p.codes_v + row * (D / 2), p.scales_v + row * (D / 16));
         gk = __ldg(p.g + 2 * sg.slot);
         gv = __ldg(p.g + 2 * sg.slot + 1);
-      } else {
-        const int key = t0 + tid;
-        const bool valid = key < sg.end;
-        const int64_t off = ((int64_t)key * H + h) * D * 2;
-        copy_row_to_smem<D>(sK, tid, (const uint8_t*)p.Kb + (valid ? off : 0), valid);
-        copy_row_to_smem<D>(sV, tid, (const uint8_t*)p.Vb + (valid ? off : 0), valid);
       }
-      fence_proxy_async_smem();
-      __syncthreads();
-      // ---- S = Q K^T  (M=128 queries, N=128 keys, K=D), fp32 in TMEM columns [0,128)
-      if (tid == 0) {
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-          umma_ss(tS, umma_desc_sw128(sQ + off, 16, 1024), umma_desc_sw128(sK + off, 16, 1024), kIdS, kk > 0);
-        }
-        tc_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
+      const float cs = gk * p.scale_log2;
+      mbar_wait(sfull + qi, j & 1);
       tc_fence_after();
-
-      // ---- online softmax on this thread's row (TMEM lane = tid)
       uint32_t s[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) KVQ_TMEM_LD32(tS + lane_off + 32 * c, (s + 32 * c));
+      for (int c = 0; c < 4; ++c) KVQ_TMEM_LD32(tS + 32 * c, (s + 32 * c));
       tmem_ld_wait();
-      const float cs = gk * p.scale_log2;
+      // row max of raw scores over valid keys (scale cs > 0 commutes with max)
       float mx = -INFINITY;
+      if (lo == 0 && hi == 128) {
 #pragma unroll
-      for (int j = 0; j < 128; ++j) {
-        const float v = (j >= lo && j < hi) ? __uint_as_float(s[j]) * cs : -INFINITY;
-        s[j] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        for (int k = 0; k < 128; k += 2) {
+          float r;
+          asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(mx), "f"(__uint_as_float(s[k])), "f"(__uint_as_float(s[k + 1])));
+          mx = r;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 128; ++k) {
+          if (k < lo || k >= hi) s[k] = __float_as_uint(-INFINITY);
+          mx = fmaxf(mx, __uint_as_float(s[k]));
+        }
       }
-      const float m_new = fmaxf(m_run, mx);
+      const float m_new = fmaxf(m_run, mx * cs);
       const float alpha = ex2_approx(m_run - m_new);
-      float lsum = 0.0f;
+      const float mneg = -m_new;
+      float lsum0 = 0.0f, lsum1 = 0.0f;
 #pragma unroll
       for (int k = 0; k < 64; ++k) {
-        const float p0 = ex2_approx(__uint_as_float(s[2 * k]) - m_new);
-        const float p1 = ex2_approx(__uint_as_float(s[2 * k + 1]) - m_new);
+        const float p0 = ex2_approx(fmaf(__uint_as_float(s[2 * k]), cs, mneg));
+        const float p1 = ex2_approx(fmaf(__uint_as_float(s[2 * k + 1]), cs, mneg));
         uint32_t pk;
         if (MMA_BF16) {
           pk = pack_bf162(p0, p1);
-          lsum += __uint_as_float(pk << 16) + __uint_as_float(pk & 0xFFFF0000u);
+          lsum0 += __uint_as_float(pk << 16);
+          lsum1 += __uint_as_float(pk & 0xFFFF0000u);
         } else {
           pk = pack_half2(p0, p1);
           __half2 hh = *reinterpret_cast<__half2*>(&pk);
-          lsum += __low2float(hh) + __high2float(hh);
+          lsum0 += __low2float(hh);
+          lsum1 += __high2float(hh);
         }
         s[k] = pk;
       }
-      l_run = l_run * alpha + lsum;
-      KVQ_TMEM_ST32(tS + lane_off, s);
-      KVQ_TMEM_ST32(tS + lane_off + 32, (s + 32));
-      // O is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new
-      if (ntile > 0) {
+      l_run = l_run * alpha + (lsum0 + lsum1);
+      KVQ_TMEM_ST32(tS, s);
+      KVQ_TMEM_ST32(tS + 32, (s + 32));
+      // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
+      // PV_i(j-1) is complete here (it was issued before QK_i(j), whose commit we waited on).
+      if (j > 0) {
         const float f = alpha * (gv_run / gv);
         if (!__all_sync(0xffffffffu, f == 1.0f)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
-            KVQ_TMEM_LD32(tO + lane_off + 32 * c, o);
+            KVQ_TMEM_LD32(tO + 32 * c, o);
             tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
-            KVQ_TMEM_ST32(tO + lane_off + 32 * c, o);
+            KVQ_TMEM_ST32(tO + 32 * c, o);
           }
         }
       }
@@ -251,30 +310,17 @@ __global__ void __launch_bounds__(128, 1) attn_kernel(const __grid_constant__ At
       m_run = m_new;
       tmem_st_wait();
       tc_fence_before();
-      __syncthreads();
-      // ---- O += P V  (A = P from TMEM columns [0,64), B = V^' MN-major in smem)
-      if (tid == 0) {
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tO, tS + 8 * kk, umma_desc_sw128(sV + kk * 2048, 16384, 1024), kIdO, (ntile > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      tc_fence_after();
-      ntile++;
+      mbar_arrive(pfull + qi);
     }
-  }
-
-  // ---- epilogue: O * g_V / l -> [Tq, H, D]
-  {
-    const int t = q0 + tid;
+    // ---- epilogue: O * g_V / l -> [Tq, H, D]
+    mbar_wait(ofull + qi, 0);
+    tc_fence_after();
+    const int t = q0 + 128 * qi + (tid & 127);
     const float f = gv_run / l_run;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t o[32];
-      KVQ_TMEM_LD32(tO + lane_off + 32 * c, o);
+      KVQ_TMEM_LD32(tO + 32 * c, o);
       tmem_ld_wait();
       if (t < p.Tq) {
         const int64_t base = ((int64_t)t * H + h) * D + 32 * c;
@@ -295,20 +341,113 @@ __global__ void __launch_bounds__(128, 1) attn_kernel(const __grid_constant__ At
         }
       }
     }
+  } else if (warp < 12) {
+    // ================================================================ dequant WG
+    reg_dealloc<kRegDequant>();
+    const int r = tid - 256;  // key row within the tile
+    TileIter it;
+    bool more = tile_first(p, it);
+    for (int j = 0; more; ++j, more = tile_next(p, it)) {
+      const AttnSeg& sg = p.seg[it.seg];
+      const int b = j & 1;
+      const uint32_t par = ((j >> 1) - 1) & 1;
+      if (NVFP4) {
+        const int64_t row = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
+        PackedRow<D> pk, pv;
+        load_packed_row<D>(pk, p.codes_k + row * (D / 2), p.scales_k + row * (D / 16));
+        load_packed_row<D>(pv, p.codes_v + row * (D / 2), p.scales_v + row * (D / 16));
+        if (j >= 2) mbar_wait(kempty + b, par);
+        store_dequant_row<D>(SK(b), r, pk);
+        fence_proxy_async_smem();
+        mbar_arrive(kfull + b);
+        if (j >= 2) mbar_wait(vempty + b, par);
+        store_dequant_row<D>(SV(b), r, pv);
+        fence_proxy_async_smem();
+        mbar_arrive(vfull + b);
+      } else {
+        const int key = it.t0 + r;
+        const bool valid = key < sg.end;
+        const int64_t off = valid ? ((int64_t)key * H + h) * D * 2 : 0;
+        if (j >= 2) mbar_wait(kempty + b, par);
+        copy_row_to_smem<D>(SK(b), r, (const uint8_t*)p.Kb + off, valid);
+        fence_proxy_async_smem();
+        mbar_arrive(kfull + b);
+        if (j >= 2) mbar_wait(vempty + b, par);
+        copy_row_to_smem<D>(SV(b), r, (const uint8_t*)p.Vb + off, valid);
+        fence_proxy_async_smem();
+        mbar_arrive(vfull + b);
+      }
+    }
+  } else {
+    reg_dealloc<kRegMma>();
+  }
+  if (tid == 12 * 32) {
+    // ================================================================ MMA issuer (one thread)
+    constexpr uint32_t kIdS = umma_idesc_f16(128, 128, MMA_BF16 ? 1 : 0, 0, 0);
+    constexpr uint32_t kIdO = umma_idesc_f16(128, D, MMA_BF16 ? 1 : 0, 0, 1);
+    auto issue_qk = [&](int qi, int b) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
+        umma_ss((tmem + 128u * qi), umma_desc_sw128(SQ(qi) + off, 16, 1024), umma_desc_sw128(SK(b) + off, 16, 1024), kIdS,
+                kk > 0 ? 1u : 0u);
+      }
+    };
+    auto issue_pv = [&](int qi, int b, bool first) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_ts((tmem + 256u + 128u * qi), (tmem + 128u * qi) + 8 * kk, umma_desc_sw128(SV(b) + kk * 2048, 16384, 1024), kIdO,
+                (!first || kk > 0) ? 1u : 0u);
+    };
+    if (ntiles > 0) {
+      mbar_wait(kfull + 0, 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      tc_commit(sfull + 0);
+      issue_qk(1, 0);
+      tc_commit(sfull + 1);
+      tc_commit(kempty + 0);
+      for (int j = 0; j < ntiles; ++j) {
+        const int b = j & 1, bn = (j + 1) & 1;
+        mbar_wait(vfull + b, (j >> 1) & 1);
+        mbar_wait(pfull + 0, j & 1);
+        tc_fence_after();
+        issue_pv(0, b, j == 0);
+        if (j + 1 < ntiles) {
+          mbar_wait(kfull + bn, ((j + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_qk(0, bn);
+          tc_commit(sfull + 0);
+        } else {
+          tc_commit(ofull + 0);
+        }
+        mbar_wait(pfull + 1, j & 1);
+        tc_fence_after();
+        issue_pv(1, b, j == 0);
+        tc_commit(vempty + b);
+        if (j + 1 < ntiles) {
+          issue_qk(1, bn);
+          tc_commit(sfull + 1);
+          tc_commit(kempty + bn);
+        } else {
+          tc_commit(ofull + 1);
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 12) tmem_dealloc(tmem, 512);
 }
 
 template <int D, bool NVFP4, bool MMA_BF16>
 cudaError_t launch_t(const AttnParams& p, cudaStream_t st) {
-  auto kern = attn_kernel<D, NVFP4, MMA_BF16>;
-  const int smem = AttnSmem<D>::kBytes;
+  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16>;
+  const int smem = WsSmem<D>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.Tq + kBM - 1) / kBM, p.H);
-  kern<<<grid, 128, smem, st>>>(p);
+  dim3 grid((p.Tq + 255) / 256, p.H);
+  kern<<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
 
