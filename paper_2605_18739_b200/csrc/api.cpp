@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t T_c, T_pad, rows_per_head;  // rows_per_head = slots * T_pad
   size_t codes_bytes, scales_bytes;   // per tensor (K or V), all layers
-  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, total;
+  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_ws, total;
 };
 
 bool valid_cfg(const kvq_config* c) {
@@ -58,6 +58,7 @@ Layout make_layout(const kvq_config* c) {
   L.off_g = off; off += align_up((size_t)c->num_layers * c->max_chunk_slots * 2 * sizeof(float), kAlign);
   L.off_partials = off; off += align_up(2 * kNumPartials * sizeof(uint32_t), kAlign);
   L.off_status = off; off += align_up(sizeof(DevStatus), kAlign);
+  L.off_ws = off; off += align_up(attn_ws_bytes(c->head_dim), kAlign);
   L.total = off;
   return L;
 }
@@ -81,6 +82,18 @@ struct kvq_cache {
 namespace {
 
 kvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? KVQ_OK : KVQ_ECUDA; }
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      n = v;
+    else
+      n = kMaxCtas;
+  }
+  return n;
+}
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 uint8_t* codes_base(const kvq_cache* c, int t, int layer) {
@@ -315,6 +328,9 @@ kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype
   p.d = d;
   const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
   p.scale_log2 = sc * 1.4426950408889634f;
+  p.ws = reinterpret_cast<float*>(c->arena + c->L.off_ws);
+  p.ws_slots = 2 * kMaxCtas;
+  p.max_ctas = std::min(sm_count(), kMaxCtas);
   return cuda_status(launch_attention(p, true, S(stream)));
 }
 

@@ -174,6 +174,53 @@ KVQ_DEV int count_tiles(const AttnParams& p) {
   return n;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent stream-K schedule.  A work UNIT is (head, pair of 128-query tiles); every unit has
+// the same n key tiles.  The U*n (unit, tile) steps are cut into gridDim.x equal contiguous
+// ranges, one per CTA (one CTA per SM), so every SM gets the same tensor-core work regardless of
+// how U compares with the SM count.  A range covers whole units (written directly) and at most
+// a partial unit at each end; a partial piece writes unnormalized O (real units), the running
+// max m (log2 domain) and the row sum l to a workspace slot: slot 2c for CTA c's first piece,
+// 2c+1 for its last, and combine_kernel merges the pieces of every split unit in a fixed order.
+struct Piece {
+  int unit, tb, te;   // unit index, tile range [tb, te)
+  bool full;          // covers the whole unit -> final output
+  int slot;           // workspace slot when !full
+};
+
+KVQ_DEV int64_t range_begin(int c, int64_t W, int G) { return (W * c) / G; }
+
+// piece k of CTA c (k = 0, 1, ...); false when past the end of the range
+KVQ_DEV bool get_piece(int c, int k, int64_t W, int G, int n, Piece& pc) {
+  const int64_t beg = range_begin(c, W, G), end = range_begin(c + 1, W, G);
+  int64_t s = beg;
+  for (int i = 0; i < k && s < end; ++i) {
+    const int64_t u = s / n;
+    s = (u + 1) * (int64_t)n < end ? (u + 1) * (int64_t)n : end;
+  }
+  if (s >= end) return false;
+  const int64_t u = s / n;
+  pc.unit = (int)u;
+  pc.tb = (int)(s - u * n);
+  const int64_t e = (u + 1) * (int64_t)n < end ? (u + 1) * (int64_t)n : end;
+  pc.te = (int)(e - u * n);
+  pc.full = (pc.tb == 0 && pc.te == n);
+  pc.slot = (s == beg) ? 2 * c : 2 * c + 1;
+  return true;
+}
+
+// position the tile iterator at tile index tb of the key-tile sequence
+KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
+  int s = 0;
+  for (; s < p.nseg; ++s) {
+    const int nt = ((p.seg[s].end + 127) >> 7) - (p.seg[s].begin >> 7);
+    if (tb < nt) break;
+    tb -= nt;
+  }
+  it.seg = s;
+  it.t0 = (p.seg[s].begin & ~127) + 128 * tb;
+}
+
 template <int D, bool NVFP4, bool MMA_BF16>
 __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
   using SM = WsSmem<D>;
@@ -186,20 +233,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #define SK(b) (sbase + (2u + (uint32_t)(b)) * kT)
 #define SV(b) (sbase + (4u + (uint32_t)(b)) * kT)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
-  uint64_t* kfull = bars + 0;   // [2]
+  uint64_t* kfull = bars + 0;   // [2] dequant -> MMA, per K^ buffer
   uint64_t* vfull = bars + 2;   // [2]
-  uint64_t* kempty = bars + 4;  // [2]
+  uint64_t* kempty = bars + 4;  // [2] MMA -> dequant
   uint64_t* vempty = bars + 6;  // [2]
-  uint64_t* sfull = bars + 8;   // [2] per query tile
-  uint64_t* pfull = bars + 10;  // [2]
-  uint64_t* ofull = bars + 12;  // [2]
+  uint64_t* sfull = bars + 8;   // [2] MMA -> softmax WG i (S_i ready; PV_i(prev) done)
+  uint64_t* pfull = bars + 10;  // [2] softmax WG i -> MMA (P_i written, O_i rescaled)
+  uint64_t* ofull = bars + 12;  // [2] MMA -> softmax WG i (last PV_i of a piece done)
+  uint64_t* qfull = bars + 14;  // [2] softmax WG i -> MMA (Q_i tile of a piece loaded)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int h = blockIdx.y;
-  const int q0 = blockIdx.x * 256;
   const int H = p.H;
-  const int ntiles = count_tiles(p);
+  const int n = count_tiles(p);
+  const int64_t W = (int64_t)p.units * n;
+  const int G = gridDim.x, c = blockIdx.x;
 
   if (warp == 12) tmem_alloc(tslot, 512);
   if (tid == 0) {
@@ -211,15 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_init(sfull + b, 1);
       mbar_init(pfull + b, 128);
       mbar_init(ofull + b, 1);
+      mbar_init(qfull + b, 128);
     }
     fence_mbar_init();
   }
-  // Q tiles (256 rows): threads 0..255 each load one row
-  if (tid < 256) {
-    const int t = q0 + tid;
-    load_q_row<D, MMA_BF16>(SQ(tid >> 7), tid & 127, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
-  }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -229,115 +272,138 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     // ================================================================ softmax WG (tile qi)
     reg_alloc<kRegSoftmax>();
     const int qi = warp >> 2;
+    const int row = tid & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + 128 * qi + lane_off;
     const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
-    float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
-    TileIter it;
-    bool more = tile_first(p, it);
-    for (int j = 0; more; ++j, more = tile_next(p, it)) {
-      const AttnSeg& sg = p.seg[it.seg];
-      const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, 128);
-      float gk = 1.0f, gv = 1.0f;
-      if (NVFP4) {
-        gk = __ldg(p.g + 2 * sg.slot);
-        gv = __ldg(p.g + 2 * sg.slot + 1);
-      }
-      const float cs = gk * p.scale_log2;
-      mbar_wait(sfull + qi, j & 1);
-      tc_fence_after();
-      uint32_t s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) KVQ_TMEM_LD32(tS + 32 * c, (s + 32 * c));
-      tmem_ld_wait();
-      // row max of raw scores over valid keys (scale cs > 0 commutes with max)
-      float mx = -INFINITY;
-      if (lo == 0 && hi == 128) {
-#pragma unroll
-        for (int k = 0; k < 128; k += 2) {
-          float r;
-          asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(mx), "f"(__uint_as_float(s[k])), "f"(__uint_as_float(s[k + 1])));
-          mx = r;
+    int g = 0;  // global tile counter (barrier parity)
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+      const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
+      const int t = q0 + 128 * qi + row;
+      load_q_row<D, MMA_BF16>(SQ(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      fence_proxy_async_smem();
+      mbar_arrive(qfull + qi);
+      float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
+      TileIter it;
+      tile_seek(p, pc.tb, it);
+      for (int j = 0; j < pc.te - pc.tb; ++j, ++g, tile_next(p, it)) {
+        const AttnSeg& sg = p.seg[it.seg];
+        const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, 128);
+        float gk = 1.0f, gv = 1.0f;
+        if (NVFP4) {
+          gk = __ldg(p.g + 2 * sg.slot);
+          gv = __ldg(p.g + 2 * sg.slot + 1);
         }
-      } else {
+        const float cs = gk * p.scale_log2;
+        mbar_wait(sfull + qi, g & 1);
+        tc_fence_after();
+        uint32_t s[128];
 #pragma unroll
-        for (int k = 0; k < 128; ++k) {
-          if (k < lo || k >= hi) s[k] = __float_as_uint(-INFINITY);
-          mx = fmaxf(mx, __uint_as_float(s[k]));
-        }
-      }
-      const float m_new = fmaxf(m_run, mx * cs);
-      const float alpha = ex2_approx(m_run - m_new);
-      const float mneg = -m_new;
-      float lsum0 = 0.0f, lsum1 = 0.0f;
+        for (int cc = 0; cc < 4; ++cc) KVQ_TMEM_LD32(tS + 32 * cc, (s + 32 * cc));
+        tmem_ld_wait();
+        // row max of raw scores over valid keys (scale cs > 0 commutes with max)
+        float mx = -INFINITY;
+        if (lo == 0 && hi == 128) {
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        const float p0 = ex2_approx(fmaf(__uint_as_float(s[2 * k]), cs, mneg));
-        const float p1 = ex2_approx(fmaf(__uint_as_float(s[2 * k + 1]), cs, mneg));
-        uint32_t pk;
-        if (MMA_BF16) {
-          pk = pack_bf162(p0, p1);
-          lsum0 += __uint_as_float(pk << 16);
-          lsum1 += __uint_as_float(pk & 0xFFFF0000u);
+          for (int kk = 0; kk < 128; kk += 2) {
+            float r;
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(mx), "f"(__uint_as_float(s[kk])), "f"(__uint_as_float(s[kk + 1])));
+            mx = r;
+          }
         } else {
-          pk = pack_half2(p0, p1);
-          __half2 hh = *reinterpret_cast<__half2*>(&pk);
-          lsum0 += __low2float(hh);
-          lsum1 += __high2float(hh);
-        }
-        s[k] = pk;
-      }
-      l_run = l_run * alpha + (lsum0 + lsum1);
-      KVQ_TMEM_ST32(tS, s);
-      KVQ_TMEM_ST32(tS + 32, (s + 32));
-      // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
-      // PV_i(j-1) is complete here (it was issued before QK_i(j), whose commit we waited on).
-      if (j > 0) {
-        const float f = alpha * (gv_run / gv);
-        if (!__all_sync(0xffffffffu, f == 1.0f)) {
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            KVQ_TMEM_LD32(tO + 32 * c, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
-            KVQ_TMEM_ST32(tO + 32 * c, o);
+          for (int kk = 0; kk < 128; ++kk) {
+            if (kk < lo || kk >= hi) s[kk] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(s[kk]));
           }
         }
+        const float m_new = fmaxf(m_run, mx * cs);
+        const float alpha = ex2_approx(m_run - m_new);
+        const float mneg = -m_new;
+        float lsum0 = 0.0f, lsum1 = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < 64; ++kk) {
+          const float p0 = ex2_approx(fmaf(__uint_as_float(s[2 * kk]), cs, mneg));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(s[2 * kk + 1]), cs, mneg));
+          uint32_t pk;
+          if (MMA_BF16) {
+            pk = pack_bf162(p0, p1);
+            lsum0 += __uint_as_float(pk << 16);
+            lsum1 += __uint_as_float(pk & 0xFFFF0000u);
+          } else {
+            pk = pack_half2(p0, p1);
+            __half2 hh = *reinterpret_cast<__half2*>(&pk);
+            lsum0 += __low2float(hh);
+            lsum1 += __high2float(hh);
+          }
+          s[kk] = pk;
+        }
+        l_run = l_run * alpha + (lsum0 + lsum1);
+        KVQ_TMEM_ST32(tS, s);
+        KVQ_TMEM_ST32(tS + 32, (s + 32));
+        // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
+        // PV_i(j-1) is complete here (issued before QK_i(j), whose commit we waited on).
+        if (j > 0) {
+          const float f = alpha * (gv_run / gv);
+          if (!__all_sync(0xffffffffu, f == 1.0f)) {
+#pragma unroll
+            for (int cc = 0; cc < D / 32; ++cc) {
+              uint32_t o[32];
+              KVQ_TMEM_LD32(tO + 32 * cc, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * f);
+              KVQ_TMEM_ST32(tO + 32 * cc, o);
+            }
+          }
+        }
+        gv_run = gv;
+        m_run = m_new;
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(pfull + qi);
       }
-      gv_run = gv;
-      m_run = m_new;
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(pfull + qi);
-    }
-    // ---- epilogue: O * g_V / l -> [Tq, H, D]
-    mbar_wait(ofull + qi, 0);
-    tc_fence_after();
-    const int t = q0 + 128 * qi + (tid & 127);
-    const float f = gv_run / l_run;
+      // ---- piece epilogue
+      mbar_wait(ofull + qi, k & 1);
+      tc_fence_after();
+      const float f = pc.full ? gv_run / l_run : gv_run;
+      float* wsO = p.ws + (size_t)pc.slot * p.ws_slot_floats + (size_t)(128 * qi + row) * D;
+      if (!pc.full && t < p.Tq) {
+        float* wml = p.ws + (size_t)pc.slot * p.ws_slot_floats + 256 * D;
+        wml[128 * qi + row] = m_run;
+        wml[256 + 128 * qi + row] = l_run;
+      }
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      KVQ_TMEM_LD32(tO + 32 * c, o);
-      tmem_ld_wait();
-      if (t < p.Tq) {
-        const int64_t base = ((int64_t)t * H + h) * D + 32 * c;
-        if (p.out_dtype == DT_FP32) {
-          float4* dst = reinterpret_cast<float4*>((float*)p.O + base);
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        KVQ_TMEM_LD32(tO + 32 * cc, o);
+        tmem_ld_wait();
+        if (t < p.Tq) {
+          if (!pc.full) {
+            float4* dst = reinterpret_cast<float4*>(wsO + 32 * cc);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            dst[k] = make_float4(__uint_as_float(o[4 * k]) * f, __uint_as_float(o[4 * k + 1]) * f,
-                                 __uint_as_float(o[4 * k + 2]) * f, __uint_as_float(o[4 * k + 3]) * f);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.O + base);
+            for (int kk = 0; kk < 8; ++kk)
+              dst[kk] = make_float4(__uint_as_float(o[4 * kk]) * f, __uint_as_float(o[4 * kk + 1]) * f,
+                                    __uint_as_float(o[4 * kk + 2]) * f, __uint_as_float(o[4 * kk + 3]) * f);
+          } else {
+            const int64_t base = ((int64_t)t * H + h) * D + 32 * cc;
+            if (p.out_dtype == DT_FP32) {
+              float4* dst = reinterpret_cast<float4*>((float*)p.O + base);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            dst[k] = make_uint4(pack_bf162(__uint_as_float(o[8 * k]) * f, __uint_as_float(o[8 * k + 1]) * f),
-                                pack_bf162(__uint_as_float(o[8 * k + 2]) * f, __uint_as_float(o[8 * k + 3]) * f),
-                                pack_bf162(__uint_as_float(o[8 * k + 4]) * f, __uint_as_float(o[8 * k + 5]) * f),
-                                pack_bf162(__uint_as_float(o[8 * k + 6]) * f, __uint_as_float(o[8 * k + 7]) * f));
+              for (int kk = 0; kk < 8; ++kk)
+                dst[kk] = make_float4(__uint_as_float(o[4 * kk]) * f, __uint_as_float(o[4 * kk + 1]) * f,
+                                      __uint_as_float(o[4 * kk + 2]) * f, __uint_as_float(o[4 * kk + 3]) * f);
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.O + base);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                dst[kk] = make_uint4(pack_bf162(__uint_as_float(o[8 * kk]) * f, __uint_as_float(o[8 * kk + 1]) * f),
+                                     pack_bf162(__uint_as_float(o[8 * kk + 2]) * f, __uint_as_float(o[8 * kk + 3]) * f),
+                                     pack_bf162(__uint_as_float(o[8 * kk + 4]) * f, __uint_as_float(o[8 * kk + 5]) * f),
+                                     pack_bf162(__uint_as_float(o[8 * kk + 6]) * f, __uint_as_float(o[8 * kk + 7]) * f));
+            }
+          }
         }
       }
     }
@@ -345,37 +411,42 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     // ================================================================ dequant WG
     reg_dealloc<kRegDequant>();
     const int r = tid - 256;  // key row within the tile
-    TileIter it;
-    bool more = tile_first(p, it);
-    for (int j = 0; more; ++j, more = tile_next(p, it)) {
-      const AttnSeg& sg = p.seg[it.seg];
-      const int b = j & 1;
-      const uint32_t par = ((j >> 1) - 1) & 1;
-      if (NVFP4) {
-        const int64_t row = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
-        PackedRow<D> pk, pv;
-        load_packed_row<D>(pk, p.codes_k + row * (D / 2), p.scales_k + row * (D / 16));
-        load_packed_row<D>(pv, p.codes_v + row * (D / 2), p.scales_v + row * (D / 16));
-        if (j >= 2) mbar_wait(kempty + b, par);
-        store_dequant_row<D>(SK(b), r, pk);
-        fence_proxy_async_smem();
-        mbar_arrive(kfull + b);
-        if (j >= 2) mbar_wait(vempty + b, par);
-        store_dequant_row<D>(SV(b), r, pv);
-        fence_proxy_async_smem();
-        mbar_arrive(vfull + b);
-      } else {
-        const int key = it.t0 + r;
-        const bool valid = key < sg.end;
-        const int64_t off = valid ? ((int64_t)key * H + h) * D * 2 : 0;
-        if (j >= 2) mbar_wait(kempty + b, par);
-        copy_row_to_smem<D>(SK(b), r, (const uint8_t*)p.Kb + off, valid);
-        fence_proxy_async_smem();
-        mbar_arrive(kfull + b);
-        if (j >= 2) mbar_wait(vempty + b, par);
-        copy_row_to_smem<D>(SV(b), r, (const uint8_t*)p.Vb + off, valid);
-        fence_proxy_async_smem();
-        mbar_arrive(vfull + b);
+    int g = 0;
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+      const int h = pc.unit / p.qpairs;
+      TileIter it;
+      tile_seek(p, pc.tb, it);
+      for (int j = pc.tb; j < pc.te; ++j, ++g, tile_next(p, it)) {
+        const AttnSeg& sg = p.seg[it.seg];
+        const int b = g & 1;
+        const uint32_t par = ((g >> 1) - 1) & 1;
+        if (NVFP4) {
+          const int64_t crow = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
+          PackedRow<D> pk, pv;
+          load_packed_row<D>(pk, p.codes_k + crow * (D / 2), p.scales_k + crow * (D / 16));
+          load_packed_row<D>(pv, p.codes_v + crow * (D / 2), p.scales_v + crow * (D / 16));
+          if (g >= 2) mbar_wait(kempty + b, par);
+          store_dequant_row<D>(SK(b), r, pk);
+          fence_proxy_async_smem();
+          mbar_arrive(kfull + b);
+          if (g >= 2) mbar_wait(vempty + b, par);
+          store_dequant_row<D>(SV(b), r, pv);
+          fence_proxy_async_smem();
+          mbar_arrive(vfull + b);
+        } else {
+          const int key = it.t0 + r;
+          const bool valid = key < sg.end;
+          const int64_t off = valid ? ((int64_t)key * H + h) * D * 2 : 0;
+          if (g >= 2) mbar_wait(kempty + b, par);
+          copy_row_to_smem<D>(SK(b), r, (const uint8_t*)p.Kb + off, valid);
+          fence_proxy_async_smem();
+          mbar_arrive(kfull + b);
+          if (g >= 2) mbar_wait(vempty + b, par);
+          copy_row_to_smem<D>(SV(b), r, (const uint8_t*)p.Vb + off, valid);
+          fence_proxy_async_smem();
+          mbar_arrive(vfull + b);
+        }
       }
     }
   } else {
@@ -389,43 +460,48 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-        umma_ss((tmem + 128u * qi), umma_desc_sw128(SQ(qi) + off, 16, 1024), umma_desc_sw128(SK(b) + off, 16, 1024), kIdS,
-                kk > 0 ? 1u : 0u);
+        umma_ss(tmem + 128u * qi, umma_desc_sw128(SQ(qi) + off, 16, 1024), umma_desc_sw128(SK(b) + off, 16, 1024),
+                kIdS, kk > 0 ? 1u : 0u);
       }
     };
     auto issue_pv = [&](int qi, int b, bool first) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
-        umma_ts((tmem + 256u + 128u * qi), (tmem + 128u * qi) + 8 * kk, umma_desc_sw128(SV(b) + kk * 2048, 16384, 1024), kIdO,
-                (!first || kk > 0) ? 1u : 0u);
+        umma_ts(tmem + 256u + 128u * qi, tmem + 128u * qi + 8 * kk, umma_desc_sw128(SV(b) + kk * 2048, 16384, 1024),
+                kIdO, (!first || kk > 0) ? 1u : 0u);
     };
-    if (ntiles > 0) {
-      mbar_wait(kfull + 0, 0);
+    int g = 0;
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+      const int np = pc.te - pc.tb;
+      mbar_wait(qfull + 0, k & 1);
+      mbar_wait(qfull + 1, k & 1);
+      mbar_wait(kfull + (g & 1), (g >> 1) & 1);
       tc_fence_after();
-      issue_qk(0, 0);
+      issue_qk(0, g & 1);
       tc_commit(sfull + 0);
-      issue_qk(1, 0);
+      issue_qk(1, g & 1);
       tc_commit(sfull + 1);
-      tc_commit(kempty + 0);
-      for (int j = 0; j < ntiles; ++j) {
-        const int b = j & 1, bn = (j + 1) & 1;
-        mbar_wait(vfull + b, (j >> 1) & 1);
-        mbar_wait(pfull + 0, j & 1);
+      tc_commit(kempty + (g & 1));
+      for (int j = 0; j < np; ++j) {
+        const int gj = g + j, b = gj & 1, bn = (gj + 1) & 1;
+        mbar_wait(vfull + b, (gj >> 1) & 1);
+        mbar_wait(pfull + 0, gj & 1);
         tc_fence_after();
         issue_pv(0, b, j == 0);
-        if (j + 1 < ntiles) {
-          mbar_wait(kfull + bn, ((j + 1) >> 1) & 1);
+        if (j + 1 < np) {
+          mbar_wait(kfull + bn, ((gj + 1) >> 1) & 1);
           tc_fence_after();
           issue_qk(0, bn);
           tc_commit(sfull + 0);
         } else {
           tc_commit(ofull + 0);
         }
-        mbar_wait(pfull + 1, j & 1);
+        mbar_wait(pfull + 1, gj & 1);
         tc_fence_after();
         issue_pv(1, b, j == 0);
         tc_commit(vempty + b);
-        if (j + 1 < ntiles) {
+        if (j + 1 < np) {
           issue_qk(1, bn);
           tc_commit(sfull + 1);
           tc_commit(kempty + bn);
@@ -433,21 +509,93 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           tc_commit(ofull + 1);
         }
       }
+      g += np;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 12) tmem_dealloc(tmem, 512);
+#undef SQ
+#undef SK
+#undef SV
+}
+
+// Merge the partial pieces of every split unit: O = sum_p 2^(m_p - m) O_p / sum_p 2^(m_p - m) l_p,
+// pieces in increasing CTA order (deterministic).  One thread per (unit row, 4 output columns).
+template <int D>
+__global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ AttnParams p, int n) {
+  const int64_t W = (int64_t)p.units * n;
+  const int G = p.grid;
+  const int tpr = D / 4;  // threads per row
+  const int64_t total = (int64_t)p.units * 256 * tpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int unit = (int)(i / (256 * tpr));
+    const int rr = (int)((i / tpr) % 256);
+    const int c4 = (int)(i % tpr);
+    const int h = unit / p.qpairs, q0 = (unit - h * p.qpairs) * 256;
+    const int t = q0 + rr;
+    if (t >= p.Tq) continue;
+    const int64_t s0 = (int64_t)unit * n, s1 = s0 + n;
+    // CTA owning step s0: largest c with range_begin(c) <= s0
+    int c0 = (int)((s0 * G) / W);
+    while (c0 + 1 < G && range_begin(c0 + 1, W, G) <= s0) ++c0;
+    while (c0 > 0 && range_begin(c0, W, G) > s0) --c0;
+    if (range_begin(c0, W, G) <= s0 && range_begin(c0 + 1, W, G) >= s1) continue;  // unsplit: written directly
+    float m = -INFINITY;
+    for (int cc = c0; cc < G && range_begin(cc, W, G) < s1; ++cc) {
+      const int slot = range_begin(cc, W, G) >= s0 ? 2 * cc : 2 * cc + 1;
+      m = fmaxf(m, p.ws[(size_t)slot * p.ws_slot_floats + 256 * D + rr]);
+    }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float l = 0.0f;
+    for (int cc = c0; cc < G && range_begin(cc, W, G) < s1; ++cc) {
+      const int slot = range_begin(cc, W, G) >= s0 ? 2 * cc : 2 * cc + 1;
+      const float* base = p.ws + (size_t)slot * p.ws_slot_floats;
+      const float w = exp2f(base[256 * D + rr] - m);
+      l += w * base[256 * D + 256 + rr];
+      const float4 o = reinterpret_cast<const float4*>(base + (size_t)rr * D)[c4];
+      acc.x += w * o.x; acc.y += w * o.y; acc.z += w * o.z; acc.w += w * o.w;
+    }
+    const float inv = 1.0f / l;
+    const int64_t ob = ((int64_t)t * p.H + h) * D + 4 * c4;
+    if (p.out_dtype == DT_FP32) {
+      *reinterpret_cast<float4*>((float*)p.O + ob) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    } else {
+      *reinterpret_cast<uint2*>((__nv_bfloat16*)p.O + ob) =
+          make_uint2(pack_bf162(acc.x * inv, acc.y * inv), pack_bf162(acc.z * inv, acc.w * inv));
+    }
+  }
 }
 
 template <int D, bool NVFP4, bool MMA_BF16>
-cudaError_t launch_t(const AttnParams& p, cudaStream_t st) {
+cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16>;
   const int smem = WsSmem<D>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.Tq + 255) / 256, p.H);
-  kern<<<grid, kThreads, smem, st>>>(p);
+  p.qpairs = (p.Tq + 255) / 256;
+  p.units = p.qpairs * p.H;
+  // persistent stream-K grid when a workspace is available, else one CTA per unit
+  int n = 0;
+  for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 127) >> 7) - (p.seg[s].begin >> 7);
+  if (n == 0 || p.units == 0) return cudaSuccess;
+  int G = p.units;
+  bool split = false;
+  if (p.ws != nullptr && p.ws_slots >= 2) {
+    G = p.ws_slots / 2 < p.max_ctas ? p.ws_slots / 2 : p.max_ctas;
+    const int64_t W = (int64_t)p.units * n;
+    if (G > W / 2) G = (int)(W / 2);  // at least two (unit, tile) steps per CTA
+    if (G < 1) G = 1;
+    split = (W % G != 0) || ((W / G) % n != 0);
+  }
+  p.grid = G;
+  p.ws_slot_floats = 256 * D + 512;
+  kern<<<G, kThreads, smem, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !split) return e;
+  const int64_t work = (int64_t)p.units * 256 * (D / 4);
+  const int cgrid = (int)((work + 255) / 256 < 148 * 8 ? (work + 255) / 256 : 148 * 8);
+  combine_kernel<D><<<cgrid, 256, 0, st>>>(p, n);
   return cudaGetLastError();
 }
 

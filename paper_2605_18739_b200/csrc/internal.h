@@ -76,9 +76,18 @@ struct AttnParams {
   const void* Vb;
   int Tq, H, d;
   float scale_log2;          // softmax_scale * log2(e)
+  // persistent stream-K schedule (filled by launch_attention)
+  float* ws;                 // partial-piece workspace (null: one CTA per unit, no partials)
+  int ws_slots;              // slots available in ws
+  int ws_slot_floats;        // floats per slot: 256 x d (O) + 512 (m, l)
+  int max_ctas;              // SM count
+  int units, qpairs, grid;
   int nseg;
   AttnSeg seg[kMaxSegs];
 };
+
+constexpr int kMaxCtas = 148;  // workspace sized for one CTA per SM on B200
+inline size_t attn_ws_bytes(int d) { return (size_t)2 * kMaxCtas * (256 * d + 512) * sizeof(float); }
 
 cudaError_t launch_amax(const void* K, const void* V, int dtype, int64_t n, uint32_t* partials,
                         DevStatus* status, cudaStream_t st);
