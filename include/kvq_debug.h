@@ -18,6 +18,13 @@
 extern "C" {
 #endif
 kvq_status kvq_debug_probe(int32_t which, const void* dev_in, void* dev_out, int64_t n, void* stream);
+
+/* Timeline instrumentation of chunk_attention: when dev_buf (>= 64*16 u64, caller-owned device
+ * memory) is set, CTA 0 of every later chunk_attention records SM clock64() at its warp-role
+ * hand-offs for its first 64 key tiles (row = tile, column = event: 0/1/2 softmax WG0 wait
+ * start / S ready / P done, 3/4/5 the same for WG1, 6/7 dequant K / V row written, 8/9/10/11
+ * MMA issue of PV0 / QK0(next) / PV1 / QK1(next) done).  NULL disables (the default). */
+kvq_status kvq_debug_set_trace(void* dev_buf);
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,8 @@ namespace {
 
 kvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? KVQ_OK : KVQ_ECUDA; }
 
+extern "C" unsigned long long* kvq_trace_ptr();
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -329,6 +331,7 @@ kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype
   const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
   p.scale_log2 = sc * 1.4426950408889634f;
   p.ws = reinterpret_cast<float*>(c->arena + c->L.off_ws);
+  p.trace = kvq_trace_ptr();
   p.ws_slots = 2 * kMaxCtas;
   p.max_ctas = std::min(sm_count(), kMaxCtas);
   return cuda_status(launch_attention(p, true, S(stream)));
@@ -526,6 +529,14 @@ kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t T
   return cuda_status(launch_ulysses_unpack_o(static_cast<const uint8_t*>(recv_buf), dtype == KVQ_BF16 ? DT_BF16 : DT_FP32,
                                              Ts, H, d, P, O_shard, S(stream)));
 }
+
+// Debug timeline buffer for chunk_attention (declared in include/kvq_debug.h)
+static unsigned long long* g_trace = nullptr;
+kvq_status kvq_debug_set_trace(void* dev_buf) {
+  g_trace = static_cast<unsigned long long*>(dev_buf);
+  return KVQ_OK;
+}
+unsigned long long* kvq_trace_ptr() { return g_trace; }
 
 // Debug probe entry point (declared in include/kvq_debug.h)
 kvq_status kvq_debug_probe(int32_t which, const void* dev_in, void* dev_out, int64_t n, void* stream) {

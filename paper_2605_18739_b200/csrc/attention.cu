@@ -221,6 +221,13 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
   it.t0 = (p.seg[s].begin & ~127) + 128 * tb;
 }
 
+// debug timeline (CTA 0, first 64 tiles): SM clock at role events, only when p.trace != null
+#define KVQ_TRACE(tile, ev)                                                                        \
+  do {                                                                                           \
+    if (p.trace != nullptr && blockIdx.x == 0 && (tile) < 64 && ((tid & 127) == 0 || tid == 384)) \
+      p.trace[(tile) * 16 + (ev)] = clock64();                                                   \
+  } while (0)
+
 template <int D, bool NVFP4, bool MMA_BF16>
 __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
   using SM = WsSmem<D>;
@@ -296,50 +303,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           gv = __ldg(p.g + 2 * sg.slot + 1);
         }
         const float cs = gk * p.scale_log2;
+        KVQ_TRACE(g, 3 * qi + 0);
         mbar_wait(sfull + qi, g & 1);
+        KVQ_TRACE(g, 3 * qi + 1);
         tc_fence_after();
         uint32_t s[128];
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) KVQ_TMEM_LD32(tS + 32 * cc, (s + 32 * cc));
         tmem_ld_wait();
         // row max of raw scores over valid keys (scale cs > 0 commutes with max)
-        float mx = -INFINITY;
-        if (lo == 0 && hi == 128) {
+        if (lo != 0 || hi != 128) {
 #pragma unroll
-          for (int kk = 0; kk < 128; kk += 2) {
-            float r;
-            asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(mx), "f"(__uint_as_float(s[kk])), "f"(__uint_as_float(s[kk + 1])));
-            mx = r;
-          }
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < 128; ++kk) {
+          for (int kk = 0; kk < 128; ++kk)
             if (kk < lo || kk >= hi) s[kk] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(s[kk]));
-          }
         }
+        // four independent 3-input max chains
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 128; kk += 8) {
+          mx0 = fmax3(mx0, __uint_as_float(s[kk]), __uint_as_float(s[kk + 1]));
+          mx1 = fmax3(mx1, __uint_as_float(s[kk + 2]), __uint_as_float(s[kk + 3]));
+          mx2 = fmax3(mx2, __uint_as_float(s[kk + 4]), __uint_as_float(s[kk + 5]));
+          mx3 = fmax3(mx3, __uint_as_float(s[kk + 6]), __uint_as_float(s[kk + 7]));
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         const float m_new = fmaxf(m_run, mx * cs);
         const float alpha = ex2_approx(m_run - m_new);
-        const float mneg = -m_new;
-        float lsum0 = 0.0f, lsum1 = 0.0f;
+        // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp32 p (two packed chains)
+        const uint64_t cs2 = f32x2_pack(cs, cs), mneg2 = f32x2_pack(-m_new, -m_new);
+        uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
         for (int kk = 0; kk < 64; ++kk) {
-          const float p0 = ex2_approx(fmaf(__uint_as_float(s[2 * kk]), cs, mneg));
-          const float p1 = ex2_approx(fmaf(__uint_as_float(s[2 * kk + 1]), cs, mneg));
-          uint32_t pk;
-          if (MMA_BF16) {
-            pk = pack_bf162(p0, p1);
-            lsum0 += __uint_as_float(pk << 16);
-            lsum1 += __uint_as_float(pk & 0xFFFF0000u);
-          } else {
-            pk = pack_half2(p0, p1);
-            __half2 hh = *reinterpret_cast<__half2*>(&pk);
-            lsum0 += __low2float(hh);
-            lsum1 += __high2float(hh);
-          }
-          s[kk] = pk;
+          const uint64_t x2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2, mneg2);
+          float x0, x1;
+          f32x2_unpack(x2, x0, x1);
+          const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+          if (kk & 1) acc1 = fadd2(acc1, f32x2_pack(p0, p1));
+          else acc0 = fadd2(acc0, f32x2_pack(p0, p1));
+          s[kk] = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
         }
-        l_run = l_run * alpha + (lsum0 + lsum1);
+        float a0, a1, b0, b1;
+        f32x2_unpack(acc0, a0, a1);
+        f32x2_unpack(acc1, b0, b1);
+        l_run = l_run * alpha + ((a0 + a1) + (b0 + b1));
         KVQ_TMEM_ST32(tS, s);
         KVQ_TMEM_ST32(tS + 32, (s + 32));
         // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
@@ -352,8 +358,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
               uint32_t o[32];
               KVQ_TMEM_LD32(tO + 32 * cc, o);
               tmem_ld_wait();
+              const uint64_t f2 = f32x2_pack(f, f);
 #pragma unroll
-              for (int kk = 0; kk < 32; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * f);
+              for (int kk = 0; kk < 32; kk += 2) {
+                float x0, x1;
+                f32x2_unpack(fmul2(f32x2_pack(__uint_as_float(o[kk]), __uint_as_float(o[kk + 1])), f2), x0, x1);
+                o[kk] = __float_as_uint(x0);
+                o[kk + 1] = __float_as_uint(x1);
+              }
               KVQ_TMEM_ST32(tO + 32 * cc, o);
             }
           }
@@ -363,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(pfull + qi);
+        KVQ_TRACE(g, 3 * qi + 2);
       }
       // ---- piece epilogue
       mbar_wait(ofull + qi, k & 1);
@@ -430,10 +443,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           store_dequant_row<D>(SK(b), r, pk);
           fence_proxy_async_smem();
           mbar_arrive(kfull + b);
+          if (r == 0) KVQ_TRACE(g, 6);
           if (g >= 2) mbar_wait(vempty + b, par);
           store_dequant_row<D>(SV(b), r, pv);
           fence_proxy_async_smem();
           mbar_arrive(vfull + b);
+          if (r == 0) KVQ_TRACE(g, 7);
         } else {
           const int key = it.t0 + r;
           const bool valid = key < sg.end;
@@ -452,23 +467,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
   } else {
     reg_dealloc<kRegMma>();
   }
-  if (tid == 12 * 32) {
-    // ================================================================ MMA issuer (one thread)
+  if (warp == 12) {
+    // ================================================================ MMA issuer warp
+    // The whole warp runs this loop converged (descriptors stay in uniform registers); one elected
+    // lane issues each unrolled group of tcgen05.mma and its commits.  Descriptor bases are
+    // precomputed; the k-step offsets are compile-time adds to the start-address field.
     constexpr uint32_t kIdS = umma_idesc_f16(128, 128, MMA_BF16 ? 1 : 0, 0, 0);
     constexpr uint32_t kIdO = umma_idesc_f16(128, D, MMA_BF16 ? 1 : 0, 0, 1);
+    const uint64_t dQ0 = umma_desc_sw128(SQ(0), 16, 1024), dQ1 = umma_desc_sw128(SQ(1), 16, 1024);
+    const uint64_t dK0 = umma_desc_sw128(SK(0), 16, 1024), dK1 = umma_desc_sw128(SK(1), 16, 1024);
+    const uint64_t dV0 = umma_desc_sw128(SV(0), 16384, 1024), dV1 = umma_desc_sw128(SV(1), 16384, 1024);
     auto issue_qk = [&](int qi, int b) {
+      const uint64_t da = qi ? dQ1 : dQ0, db = b ? dK1 : dK0;
+      const uint32_t dt = tmem + 128u * qi;
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-        umma_ss(tmem + 128u * qi, umma_desc_sw128(SQ(qi) + off, 16, 1024), umma_desc_sw128(SK(b) + off, 16, 1024),
-                kIdS, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+          umma_ss(dt, da + off, db + off, kIdS, kk > 0 ? 1u : 0u);
+        }
       }
+      __syncwarp();
     };
     auto issue_pv = [&](int qi, int b, bool first) {
+      const uint64_t db = b ? dV1 : dV0;
+      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + 128u * qi;
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        umma_ts(tmem + 256u + 128u * qi, tmem + 128u * qi + 8 * kk, umma_desc_sw128(SV(b) + kk * 2048, 16384, 1024),
-                kIdO, (!first || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ts(dt, ta + 8 * kk, db + (uint64_t)((kk * 2048) >> 4), kIdO, (!first || kk > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto tc_commit = [&](uint64_t* bar) {
+      if (elect_one()) kvq::tc_commit(bar);
+      __syncwarp();
     };
     int g = 0;
     Piece pc;
@@ -488,10 +521,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         mbar_wait(vfull + b, (gj >> 1) & 1);
         mbar_wait(pfull + 0, gj & 1);
         tc_fence_after();
+        KVQ_TRACE(gj, 8);
         issue_pv(0, b, j == 0);
         if (j + 1 < np) {
           mbar_wait(kfull + bn, ((gj + 1) >> 1) & 1);
           tc_fence_after();
+          KVQ_TRACE(gj + 1, 9);
           issue_qk(0, bn);
           tc_commit(sfull + 0);
         } else {
@@ -499,10 +534,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         }
         mbar_wait(pfull + 1, gj & 1);
         tc_fence_after();
+        KVQ_TRACE(gj, 10);
         issue_pv(1, b, j == 0);
         tc_commit(vempty + b);
         if (j + 1 < np) {
           issue_qk(1, bn);
+          KVQ_TRACE(gj + 1, 11);
           tc_commit(sfull + 1);
           tc_commit(kempty + bn);
         } else {

@@ -116,6 +116,12 @@ KVQ_DEV void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {   // whole warp
 KVQ_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {      // whole warp
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// true on exactly one (the lowest active) lane of a converged warp
+KVQ_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{ .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}" : "=r"(pred));
+  return pred != 0;
+}
 KVQ_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 KVQ_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 KVQ_DEV void tc_commit(uint64_t* bar) {
@@ -192,6 +198,34 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, int ab_bf16,
 // Byte offset of 16-byte chunk `c16` (0..7) of row `r` inside a 128B-swizzled atom stack
 // (rows 128 B apart, 8-row atoms of 1024 B): Swizzle<3,4,3>.
 KVQ_DEV uint32_t sw128_off(uint32_t r, uint32_t c16) { return r * 128u + ((c16 ^ (r & 7u)) << 4); }
+
+// packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 process two fp32 lanes per instruction)
+KVQ_DEV uint64_t f32x2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+KVQ_DEV void f32x2_unpack(uint64_t v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+KVQ_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+KVQ_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+KVQ_DEV uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+KVQ_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 
 KVQ_DEV float ex2_approx(float x) {
   float y;

@@ -77,6 +77,7 @@ struct AttnParams {
   int Tq, H, d;
   float scale_log2;          // softmax_scale * log2(e)
   // persistent stream-K schedule (filled by launch_attention)
+  unsigned long long* trace; // debug timeline of CTA 0 (null in production)
   float* ws;                 // partial-piece workspace (null: one CTA per unit, no partials)
   int ws_slots;              // slots available in ws
   int ws_slot_floats;        // floats per slot: 256 x d (O) + 512 (m, l)

@@ -86,6 +86,7 @@ _SIGS = {
     "kvq_ulysses_unpack_o": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, _P, _P]),
     "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
+    "kvq_debug_set_trace": (ctypes.c_int, [_P]),
 }
 
 
