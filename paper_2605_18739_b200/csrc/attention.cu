@@ -37,6 +37,12 @@ constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant,
 // Register budget per SM sub-partition (16K regs = 4 warps x 128 at launch), rebalanced with
 // setmaxnreg: softmax 176 + 176, dequant 80, MMA warpgroup 80 (sum 512 per thread slot).
 constexpr int kRegSoftmax = 176, kRegDequant = 80, kRegMma = 80;
+// Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
+// FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
+#ifndef KVQ_POLY_PAIRS
+#define KVQ_POLY_PAIRS 1
+#endif
+constexpr int kPolyPairs = KVQ_POLY_PAIRS;
 
 template <int N>
 KVQ_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -104,8 +110,7 @@ KVQ_DEV void store_dequant_row(uint32_t base, int r, const PackedRow<D>& pr) {
       const uint4 q = pr.c[wi >> 2];
       const uint32_t w = (wi & 3) == 0 ? q.x : (wi & 3) == 1 ? q.y : (wi & 3) == 2 ? q.z : q.w;
       uint32_t o[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) o[b] = hmul2_u32(f16x2_from_e2m1x2((w >> (8 * b)) & 0xFF), s2);
+      dequant_word_f16(w, s2, o);
       st_shared_v4(chunk_addr(base, r, wi), o[0], o[1], o[2], o[3]);
     }
   }
@@ -335,9 +340,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #pragma unroll
         for (int kk = 0; kk < 64; ++kk) {
           const uint64_t x2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2, mneg2);
-          float x0, x1;
+          float x0, x1, p0, p1;
           f32x2_unpack(x2, x0, x1);
-          const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+          if ((kk & 7) < kPolyPairs) {  // a fixed share of the exponentials on the FMA pipe
+            exp2_poly_pair(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_approx(x0);
+            p1 = ex2_approx(x1);
+          }
           if (kk & 1) acc1 = fadd2(acc1, f32x2_pack(p0, p1));
           else acc0 = fadd2(acc0, f32x2_pack(p0, p1));
           s[kk] = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
@@ -353,20 +363,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         if (j > 0) {
           const float f = alpha * (gv_run / gv);
           if (!__all_sync(0xffffffffu, f == 1.0f)) {
+            // two 32-column chunks per TMEM round trip, staged in the free half of s[]
+            const uint64_t f2 = f32x2_pack(f, f);
 #pragma unroll
-            for (int cc = 0; cc < D / 32; ++cc) {
-              uint32_t o[32];
+            for (int cc = 0; cc < D / 32; cc += 2) {
+              uint32_t* o = s + 64;
               KVQ_TMEM_LD32(tO + 32 * cc, o);
+              if (D / 32 > 1) KVQ_TMEM_LD32(tO + 32 * (cc + 1), (o + 32));
               tmem_ld_wait();
-              const uint64_t f2 = f32x2_pack(f, f);
 #pragma unroll
-              for (int kk = 0; kk < 32; kk += 2) {
+              for (int kk = 0; kk < (D / 32 > 1 ? 64 : 32); kk += 2) {
                 float x0, x1;
                 f32x2_unpack(fmul2(f32x2_pack(__uint_as_float(o[kk]), __uint_as_float(o[kk + 1])), f2), x0, x1);
                 o[kk] = __float_as_uint(x0);
                 o[kk + 1] = __float_as_uint(x1);
               }
               KVQ_TMEM_ST32(tO + 32 * cc, o);
+              if (D / 32 > 1) KVQ_TMEM_ST32(tO + 32 * (cc + 1), (o + 32));
             }
           }
         }

@@ -47,6 +47,18 @@ KVQ_DEV float e4m3_to_f32(uint32_t byte) {
   return __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFF)));
 }
 
+// 8 E2M1 codes (one 32-bit word, element 2k in the low nibble of byte k) times a f16x2 scale
+// pair -> 4 f16x2 words, exact.  The byte split is a register-vector move, so ptxas feeds the
+// four F2FP.E2M1.UNPACK_B instructions with byte selectors (no shift/mask instructions).
+KVQ_DEV void dequant_word_f16(uint32_t w, uint32_t s2, uint32_t (&o)[4]) {
+  asm("{ .reg .b8 b0, b1, b2, b3;\n .reg .b32 h0, h1, h2, h3;\n mov.b32 {b0, b1, b2, b3}, %4;\n"
+      " cvt.rn.f16x2.e2m1x2 h0, b0;\n cvt.rn.f16x2.e2m1x2 h1, b1;\n cvt.rn.f16x2.e2m1x2 h2, b2;\n"
+      " cvt.rn.f16x2.e2m1x2 h3, b3;\n mul.rn.f16x2 %0, h0, %5;\n mul.rn.f16x2 %1, h1, %5;\n"
+      " mul.rn.f16x2 %2, h2, %5;\n mul.rn.f16x2 %3, h3, %5;\n}"
+      : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3])
+      : "r"(w), "r"(s2));
+}
+
 KVQ_DEV uint32_t hmul2_u32(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -225,6 +237,27 @@ KVQ_DEV float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
+}
+
+// 2^x for a pair of x <= 0 on the FMA pipe (offloads the MUFU unit): x = j + r, j = rint(x) via
+// the 1.5*2^23 magic add, r in [-1/2, 1/2]; 2^r by a degree-3 polynomial (relative error <= 1.0e-4,
+// below the fp16 half-ulp 2^-11 that P is rounded to), 2^j by adding j to the exponent field.
+// x is clamped at -127 (2^-127 flushes to 0 in fp16; masked keys pass -inf).
+KVQ_DEV void exp2_poly_pair(float x0, float x1, float& y0, float& y1) {
+  const uint64_t xm = f32x2_pack(fmaxf(x0, -127.0f), fmaxf(x1, -127.0f));
+  const uint64_t magic = f32x2_pack(12582912.0f, 12582912.0f);
+  const uint64_t t = fadd2(xm, magic);                                        // RN to integer in low bits
+  const uint64_t j = fadd2(t, f32x2_pack(-12582912.0f, -12582912.0f));        // rint(x)
+  const uint64_t r = ffma2(j, f32x2_pack(-1.0f, -1.0f), xm);                  // x - rint(x)
+  uint64_t p = ffma2(r, f32x2_pack(0.05500861629843712f, 0.05500861629843712f),
+                     f32x2_pack(0.24221020936965942f, 0.24221020936965942f));
+  p = ffma2(p, r, f32x2_pack(0.6932829022407532f, 0.6932829022407532f));
+  p = ffma2(p, r, f32x2_pack(1.0f, 1.0f));
+  float p0, p1, t0, t1;
+  f32x2_unpack(p, p0, p1);
+  f32x2_unpack(t, t0, t1);
+  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
 
 KVQ_DEV float ex2_approx(float x) {
