@@ -25,6 +25,10 @@ kvq_status kvq_debug_probe(int32_t which, const void* dev_in, void* dev_out, int
  * start / S ready / P done, 3/4/5 the same for WG1, 6/7 dequant K / V row written, 8/9/10/11
  * MMA issue of PV0 / QK0(next) / PV1 / QK1(next) done).  NULL disables (the default). */
 kvq_status kvq_debug_set_trace(void* dev_buf);
+
+/* on != 0: kv_quantize_append always uses the two-launch path (amax pass + quantize pass) instead
+ * of the single-pass cooperative kernel, so tests can check both produce identical bytes. */
+kvq_status kvq_debug_force_two_pass(kvq_cache* cache, int32_t on);
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t T_c, T_pad, rows_per_head;  // rows_per_head = slots * T_pad
   size_t codes_bytes, scales_bytes;   // per tensor (K or V), all layers
-  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_ws, total;
+  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_counters, off_ws, total;
 };
 
 bool valid_cfg(const kvq_config* c) {
@@ -58,6 +58,8 @@ Layout make_layout(const kvq_config* c) {
   L.off_g = off; off += align_up((size_t)c->num_layers * c->max_chunk_slots * 2 * sizeof(float), kAlign);
   L.off_partials = off; off += align_up(2 * kNumPartials * sizeof(uint32_t), kAlign);
   L.off_status = off; off += align_up(sizeof(DevStatus), kAlign);
+  L.off_counters = off;  // grid-barrier slots of the single-pass quantizer: [CTA][K|V] u64
+  off += align_up((size_t)2 * kNumPartials * sizeof(unsigned long long), kAlign);
   L.off_ws = off; off += align_up(attn_ws_bytes(c->head_dim), kAlign);
   L.total = off;
   return L;
@@ -77,6 +79,8 @@ struct kvq_cache {
   uint8_t* arena;
   std::vector<LayerState> layers;
   int64_t shot_start = 0, shot_len = 0;
+  bool two_pass_only = false;  // debug: force the amax + quantize two-pass path
+  unsigned long long quant_epoch = 0;  // single-pass quantizer launches since the arena was zeroed
 };
 
 namespace {
@@ -112,6 +116,7 @@ DevStatus* status_ptr(const kvq_cache* c) { return reinterpret_cast<DevStatus*>(
 kvq_status reset_device(kvq_cache* c, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(c->arena, 0, c->L.total, st);
   if (e != cudaSuccess) return KVQ_ECUDA;
+  c->quant_epoch = 0;  // the grid-barrier counters were zeroed with the arena
   DevStatus init{0, 0, ~0ull};
   // status word: code 0, first_bad = max (a small H2D copy from a static host value)
   static DevStatus s_init = init;
@@ -205,10 +210,6 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   const int64_t rows = c->L.T_c * H;
   cudaStream_t st = S(stream);
   uint32_t* partials = reinterpret_cast<uint32_t*>(c->arena + c->L.off_partials);
-  if (!ext_amax) {
-    cudaError_t e = launch_amax(K, V, dt == KVQ_BF16 ? DT_BF16 : DT_FP32, rows * d, partials, status_ptr(c), st);
-    if (e != cudaSuccess) return KVQ_ECUDA;
-  }
   QuantParams p{};
   p.x[0] = K;
   p.x[1] = V;
@@ -225,7 +226,21 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   p.partials = ext_amax ? nullptr : partials;
   p.ext_amax = ext_amax;
   p.status = status_ptr(c);
-  cudaError_t e = launch_quantize(p, st);
+  p.trace = kvq_trace_ptr();
+  p.epoch = c->quant_epoch;
+  // single pass when the chunk fits in aggregate shared memory, else amax pass + quantize pass
+  cudaError_t e = c->two_pass_only ? cudaErrorNotSupported
+                                   : launch_quantize_fused(p, reinterpret_cast<unsigned long long*>(c->arena + c->L.off_counters),
+                                                           partials, sm_count(), st);
+  if (e == cudaSuccess && !ext_amax) c->quant_epoch++;  // the launch arrives G times on each counter
+  if (e == cudaErrorNotSupported) {
+    (void)cudaGetLastError();
+    if (!ext_amax) {
+      e = launch_amax(K, V, dt == KVQ_BF16 ? DT_BF16 : DT_FP32, rows * d, partials, status_ptr(c), st);
+      if (e != cudaSuccess) return KVQ_ECUDA;
+    }
+    e = launch_quantize2(p, sm_count(), st);
+  }
   if (e != cudaSuccess) return KVQ_ECUDA;
   ls.slot_of[chunk] = slot;
   ls.chunk_in[slot] = chunk;
@@ -528,6 +543,12 @@ kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t T
   if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
   return cuda_status(launch_ulysses_unpack_o(static_cast<const uint8_t*>(recv_buf), dtype == KVQ_BF16 ? DT_BF16 : DT_FP32,
                                              Ts, H, d, P, O_shard, S(stream)));
+}
+
+kvq_status kvq_debug_force_two_pass(kvq_cache* c, int32_t on) {
+  if (!c) return KVQ_EINVAL;
+  c->two_pass_only = on != 0;
+  return KVQ_OK;
 }
 
 // Debug timeline buffer for chunk_attention (declared in include/kvq_debug.h)

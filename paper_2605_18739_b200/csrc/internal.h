@@ -28,6 +28,8 @@ struct QuantParams {
   float* g_out;              // [2]: K, V tensor scales of this (layer, slot)
   const uint32_t* partials;  // [2][kNumPartials] amax bit patterns, or null
   const float* ext_amax;     // [2] caller-supplied amax (Ulysses), or null
+  unsigned long long* trace; // debug timeline (null in production)
+  unsigned long long epoch;  // single-pass launches so far on this cache (grid-barrier target)
   DevStatus* status;
 };
 
@@ -93,6 +95,11 @@ inline size_t attn_ws_bytes(int d) { return (size_t)2 * kMaxCtas * (256 * d + 51
 cudaError_t launch_amax(const void* K, const void* V, int dtype, int64_t n, uint32_t* partials,
                         DevStatus* status, cudaStream_t st);
 cudaError_t launch_quantize(const QuantParams& p, cudaStream_t st);
+// second pass of the two-launch path (after launch_amax), deferred-exact per-block work
+cudaError_t launch_quantize2(const QuantParams& p, int sms, cudaStream_t st);
+// single-pass cooperative quantize/append; cudaErrorNotSupported when the chunk does not fit
+cudaError_t launch_quantize_fused(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,
+                                  cudaStream_t st);
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t st);
 cudaError_t launch_export(const ExportParams& p, cudaStream_t st);
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st);

@@ -132,8 +132,125 @@ KVQ_DEV void load_block16(const uint8_t* src, float (&x)[16]) {
   }
 }
 
+// Four E2M1 code bytes (8 elements, element 2k in the low nibble) from four fp32 pairs: ptxas merges
+// the four cvt.rn.satfinite.e2m1x2 results into one register (F2FP ... PACK_AB_MERGE_C).
+KVQ_DEV uint32_t e2m1x8(const float* q) {
+  uint32_t r;
+  asm("{ .reg .b8 e0, e1, e2, e3;\n cvt.rn.satfinite.e2m1x2.f32 e0, %2, %1;\n cvt.rn.satfinite.e2m1x2.f32 e1, %4, %3;\n"
+      " cvt.rn.satfinite.e2m1x2.f32 e2, %6, %5;\n cvt.rn.satfinite.e2m1x2.f32 e3, %8, %7;\n mov.b32 %0, {e0, e1, e2, e3};\n}"
+      : "=r"(r)
+      : "f"(q[0]), "f"(q[1]), "f"(q[2]), "f"(q[3]), "f"(q[4]), "f"(q[5]), "f"(q[6]), "f"(q[7]));
+  return r;
+}
+
+// One 16-element block, definition R1 (reading Z4):
+//   s = E4M3_RNE_SAT(RN32(RN32(bmax / g) / 6)) (0 -> 2^-9; zero block -> 0x00, codes 0x00),
+//   d_b = RN32(dec(s) * g),  c = E2M1_RNE_SAT(RN32(x / d_b)).
+// The per-element quotient uses a per-block reciprocal r = RN32(1/d_b) and one FMA correction
+// (q0 = x r, e = x - q0 d_b exact, q1 = q0 + e r; packed fp32x2), which is within 1 ulp of
+// RN32(x/d_b).  The E2M1 code of q1 can then differ from the code of RN32(x/d_b) only if q1 lies
+// within 1 ulp of an E2M1 rounding midpoint (0.25, 0.75, ..., 5 -- all <= 3 significant bits), so
+// every quotient within [-2, +5] ulps of ANY value with <= 3 significant bits (mantissa bits below
+// the top two in {-2..5} mod 2^21) sends the whole block through exact __fdiv_rn.  The result is
+// bit-identical to the correctly rounded definition; the guard fires for ~4e-6 of random quotients
+// (and for exact lattice values / zeros, which simply take the slow path).
+KVQ_DEV float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// a / b within 1 ulp of RN32(a/b), given rb ~ 1/b (relative error <~ 2^-22): q0 = a*rb, then one
+// FMA residual correction.
+KVQ_DEV float div_corrected(float a, float b, float rb) {
+  const float q0 = __fmul_rn(a, rb);
+  return __fmaf_rn(__fmaf_rn(-q0, b, a), rb, q0);
+}
+
+// NB blocks at once (independent instruction streams for latency hiding).  The scale uses the
+// same idea as the codes: u1 ~ RN32(RN32(bmax/g)/6) is within 3 ulps of the exact value, and the
+// E4M3 rounding decision can only differ when u1 lies within 3 ulps of an E4M3 midpoint (<= 5
+// significant bits), detected from the 19 mantissa bits below the top four; such blocks recompute
+// t and u with __fdiv_rn.
+// Fast path for NB blocks; bit b of the return value is set when block b's scale or one of its
+// codes might differ from the exact definition -- the caller then recomputes that block with
+// quantize_block16_exact (deferred, so the rare exact path does not stall whole warps).
+template <int NB>
+KVQ_DEV uint32_t quantize_blocks_fast(const float (&v)[NB][16], float g, float rg, uint32_t (&sbyte)[NB],
+                                      uint32_t (&w0)[NB], uint32_t (&w1)[NB]) {
+  uint32_t flags = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float m0 = 0.0f, m1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 16; k += 4) {
+      m0 = fmax3(m0, fabsf(v[b][k]), fabsf(v[b][k + 1]));
+      m1 = fmax3(m1, fabsf(v[b][k + 2]), fabsf(v[b][k + 3]));
+    }
+    const float bmax = fmaxf(m0, m1);
+    const float u = div_corrected(div_corrected(bmax, g, rg), 6.0f, 0.16666667163372040f);
+    uint32_t mn = (__float_as_uint(u) + 4u) & 0x7FFF8u;  // 0 <=> u near an E4M3 midpoint
+    uint32_t s = e4m3_from_f32(u);
+    if (s == 0) s = 1;                          // SPEC.md:191 underflow promotion
+    if (!(bmax > 0.0f)) s = 0;                  // zero block (reading Z5)
+    sbyte[b] = s;
+    const float db = __fmul_rn(e4m3_to_f32(s), g);  // decode scale of Eq. 2
+    const float r = rcp_approx(db);
+    const uint64_t r2 = f32x2_pack(r, r), nd2 = f32x2_pack(-db, -db);
+    float q[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t x2 = f32x2_pack(v[b][2 * k], v[b][2 * k + 1]);
+      const uint64_t q0 = fmul2(x2, r2);
+      const uint64_t e = ffma2(q0, nd2, x2);  // x - q0 * d_b
+      const uint64_t q1 = ffma2(e, r2, q0);
+      f32x2_unpack(q1, q[2 * k], q[2 * k + 1]);
+      mn = min(mn, (__float_as_uint(q[2 * k]) + 2u) & 0x1FFFF8u);  // 0 <=> q near an E2M1 midpoint
+      mn = min(mn, (__float_as_uint(q[2 * k + 1]) + 2u) & 0x1FFFF8u);
+    }
+    w0[b] = e2m1x8(q);
+    w1[b] = e2m1x8(q + 8);
+    if (s == 0) w0[b] = w1[b] = 0u;
+    if (mn == 0 && s != 0) flags |= 1u << b;
+  }
+  return flags;
+}
+
+// The definition itself, with IEEE divisions (reading Z4, R1): the reference path for flagged
+// blocks and for the two-pass fallback.
+KVQ_DEV void quantize_block16_exact(const float (&v)[16], float g, uint32_t& sbyte, uint32_t& w0, uint32_t& w1) {
+  float bmax = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) bmax = fmaxf(bmax, fabsf(v[k]));
+  sbyte = 0;
+  w0 = 0;
+  w1 = 0;
+  if (!(bmax > 0.0f)) return;
+  sbyte = e4m3_from_f32(__fdiv_rn(__fdiv_rn(bmax, g), 6.0f));
+  if (sbyte == 0) sbyte = 1;
+  const float db = __fmul_rn(e4m3_to_f32(sbyte), g);
+  float q[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) q[k] = __fdiv_rn(v[k], db);
+  w0 = e2m1x8(q);
+  w1 = e2m1x8(q + 8);
+}
+
+KVQ_DEV void quantize_block16(const float (&v)[16], float g, uint32_t& sbyte, uint32_t& w0, uint32_t& w1) {
+  float vv[1][16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) vv[0][k] = v[k];
+  uint32_t s[1], a[1], b[1];
+  if (quantize_blocks_fast<1>(vv, g, rcp_approx(g), s, a, b)) {
+    quantize_block16_exact(v, g, sbyte, w0, w1);
+    return;
+  }
+  sbyte = s[0];
+  w0 = a[0];
+  w1 = b[0];
+}
+
 template <int DT, int D>
-__global__ void __launch_bounds__(256) quant_kernel(const QuantParams p) {
+__global__ void __launch_bounds__(256) quant_kernel(const __grid_constant__ QuantParams p) {
   constexpr int kNB = D / 16;                 // blocks per row
   constexpr int kES = DT == DT_BF16 ? 2 : 4;  // input element bytes
   const int tsr = blockIdx.y;
@@ -171,24 +288,8 @@ __global__ void __launch_bounds__(256) quant_kernel(const QuantParams p) {
     const int j = (int)(b - row * kNB);
     float v[16];
     load_block16<DT>(x + (row * D + j * 16) * kES, v);
-    float bmax = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) bmax = fmaxf(bmax, fabsf(v[k]));
-    uint32_t sbyte = 0, w0 = 0, w1 = 0;
-    if (bmax > 0.0f) {
-      // R1: t = RN32(bmax/g); u = RN32(t/6); s = E4M3_RNE_SAT(u); s = 0 -> 2^-9
-      const float t = __fdiv_rn(bmax, g);
-      const float u = __fdiv_rn(t, 6.0f);
-      sbyte = e4m3_from_f32(u);
-      if (sbyte == 0) sbyte = 1;
-      // decode scale of Eq. 2: d_b = RN32(dec(s) * g); codes E2M1_RNE_SAT(RN32(x / d_b))
-      const float db = __fmul_rn(e4m3_to_f32(sbyte), g);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        w0 |= e2m1x2_from_f32(__fdiv_rn(v[2 * k], db), __fdiv_rn(v[2 * k + 1], db)) << (8 * k);
-        w1 |= e2m1x2_from_f32(__fdiv_rn(v[8 + 2 * k], db), __fdiv_rn(v[8 + 2 * k + 1], db)) << (8 * k);
-      }
-    }  // zero block: scale 0x00, codes 0x00 (reading Z5)
+    uint32_t sbyte, w0, w1;
+    quantize_block16(v, g, sbyte, w0, w1);
     const int t_tok = (int)(row / p.H);
     const int h = (int)(row - (int64_t)t_tok * p.H);
     const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
@@ -197,10 +298,270 @@ __global__ void __launch_bounds__(256) quant_kernel(const QuantParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Single-pass quantize/append (the default when the chunk fits in aggregate shared memory): a
+// cooperative persistent grid, one CTA per SM.  Each CTA bulk-copies (TMA engine, one
+// cp.async.bulk per tensor) its contiguous slice of K and of V -- 194 KB per SM for the Wan chunk --
+// into shared memory, so HBM is read exactly once.  Per tensor: local amax from smem -> partial ->
+// grid barrier (monotonic counter, no reset) -> every CTA reduces the partials to g -> quantizes its
+// slice from smem.  K is quantized while V is still landing.
+#ifndef KVQ_QUANT_THREADS
+#define KVQ_QUANT_THREADS 512
+#endif
+#ifndef KVQ_QUANT_NB
+#define KVQ_QUANT_NB 2
+#endif
+constexpr int kFusedThreads = KVQ_QUANT_THREADS;
+constexpr int kQNB = KVQ_QUANT_NB;  // blocks per thread per iteration
+
+template <int DT>
+KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
+  uint32_t m = 0;
+  const uint32_t base = smem_u32(s);  // explicit ld.shared (LDS.128), four vectors in flight
+  int i = threadIdx.x * 16;
+  for (; i + 3 * kFusedThreads * 16 < nbytes; i += 4 * kFusedThreads * 16) {
+    const uint4 a = ld_shared_v4(base + i), b = ld_shared_v4(base + i + kFusedThreads * 16);
+    const uint4 c = ld_shared_v4(base + i + 2 * kFusedThreads * 16), d = ld_shared_v4(base + i + 3 * kFusedThreads * 16);
+    m = max(m, max(max(vec_absmax_bits<DT>(a), vec_absmax_bits<DT>(b)), max(vec_absmax_bits<DT>(c), vec_absmax_bits<DT>(d))));
+  }
+  for (; i < nbytes; i += kFusedThreads * 16) m = max(m, vec_absmax_bits<DT>(ld_shared_v4(base + i)));
+  return m;
+}
+
+// debug timeline (globaltimer ns) of CTA 0 (slots 0-7) and the last CTA (8-15) when p.trace is set
+#define QTRACE(ev)                                                                       \
+  do {                                                                                   \
+    if (p.trace != nullptr && tid == 0 && c < 256) {                                     \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      p.trace[c * 8 + (ev)] = t_;                                                        \
+    }                                                                                    \
+  } while (0)
+
+// STAGED = true: the single-pass cooperative kernel described above.  STAGED = false: the second
+// pass of the two-launch path -- same per-block work, data read from global memory (L2-resident
+// after the amax pass), tensor amax reduced from the amax kernel's partials, ordinary launch.
+template <int DT, int D, bool STAGED>
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    quant_fused_kernel(const __grid_constant__ QuantParams p, unsigned long long* slots, int upc) {
+  const unsigned long long epoch = p.epoch;
+  constexpr int kNB = D / 16;
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);  // bytes per 16-element block
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t red[kFusedThreads / 32];
+  __shared__ uint32_t s_amax;
+  __shared__ int s_nq;
+  const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  const int64_t NU = (int64_t)p.rows * kNB;
+  const int64_t u0 = (int64_t)c * upc;
+  const int64_t left = NU - u0;
+  const int nu = left <= 0 ? 0 : (left < upc ? (int)left : upc);
+  const uint32_t slice = (uint32_t)upc * kUB;  // the V slice follows the K slice in smem
+  // flagged block indices [upc]
+  uint32_t* queue = reinterpret_cast<uint32_t*>(STAGED ? sm + 2 * (size_t)slice : sm);
+  if (tid == 0) {
+    s_nq = 0;
+    mbar_init(bar + 0, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (STAGED && tid == 0 && nu > 0) {
+    for (int t = 0; t < 2; ++t) {
+      mbar_arrive_expect_tx(bar + t, (uint32_t)nu * kUB);
+      bulk_g2s(sm + t * slice, (const uint8_t*)p.x[t] + u0 * kUB, (uint32_t)nu * kUB, bar + t);
+    }
+  }
+  QTRACE(0);
+  // ---- global amax of K and of V: one grid barrier for both tensors.  Each CTA max-reduces its
+  // two slices from smem, then (thread 0) a fire-and-forget red.max into this launch's amax words
+  // (double-buffered by launch parity; the other pair is cleared for the next launch) and one
+  // release-add on a monotonic arrival counter; epoch = earlier single-pass launches on this cache
+  // (host-tracked), so the barrier target is known without reading the counter first.
+  __shared__ uint32_t s_am[2];
+  if (STAGED && nu > 0) {
+    mbar_wait(bar + 0, 0);
+    mbar_wait(bar + 1, 0);
+  }
+  QTRACE(1);
+  if (p.ext_amax) {
+    if (tid < 2) s_am[tid] = __float_as_uint(p.ext_amax[tid]) & 0x7FFFFFFFu;
+    __syncthreads();
+  } else if (!STAGED) {  // reduce the amax kernel's per-CTA partials
+    uint32_t mk = 0, mv = 0;
+    for (int k = tid; k < kNumPartials; k += kFusedThreads) {
+      mk = max(mk, p.partials[k]);
+      mv = max(mv, p.partials[kNumPartials + k]);
+    }
+    mk = warp_max_u32(mk);
+    mv = warp_max_u32(mv);
+    if ((tid & 31) == 0) {
+      red[tid >> 5] = mk;
+      queue[tid >> 5] = mv;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      mk = 0;
+      mv = 0;
+      for (int w = 0; w < kFusedThreads / 32; ++w) {
+        mk = max(mk, red[w]);
+        mv = max(mv, queue[w]);
+      }
+      s_am[0] = mk;
+      s_am[1] = mv;
+    }
+    __syncthreads();
+  } else {
+    uint32_t mk = warp_max_u32(smem_absmax<DT>(sm, nu * kUB));
+    uint32_t mv = warp_max_u32(smem_absmax<DT>(sm + slice, nu * kUB));
+    if ((tid & 31) == 0) red[tid >> 5] = mk;
+    if ((tid & 31) == 0) queue[tid >> 5] = mv;  // queue is free until the quantize loop
+    __syncthreads();
+    // Barrier without fences or atomics: CTA c publishes (epoch tag << 32 | max) for K and for V as
+    // single 64-bit stores (tag and value become visible together); then G threads of every CTA
+    // each poll one publisher's slot until its tag is this launch's epoch, and the CTA max-reduces.
+    const uint32_t tag = (uint32_t)(epoch + 1);
+    QTRACE(5);
+    if (tid == 0) {
+      mk = 0;
+      mv = 0;
+      for (int w = 0; w < kFusedThreads / 32; ++w) {
+        mk = max(mk, red[w]);
+        mv = max(mv, queue[w]);
+      }
+      const unsigned long long vk = ((unsigned long long)tag << 32) | mk, vv = ((unsigned long long)tag << 32) | mv;
+      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slots + 2 * c), "l"(vk), "l"(vv) : "memory");
+    }
+    mk = 0;
+    mv = 0;
+    if (tid < 32) {  // one warp polls (limits the polling traffic to 32 loads in flight per CTA)
+      for (int k = tid; k < G; k += 32) {
+        unsigned long long a, b;
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(slots + 2 * k) : "memory");
+          if ((uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag) break;
+          __nanosleep(64);
+        }
+        mk = max(mk, (uint32_t)a);
+        mv = max(mv, (uint32_t)b);
+      }
+    }
+    QTRACE(6);
+    mk = warp_max_u32(mk);
+    mv = warp_max_u32(mv);
+    __syncthreads();
+    if ((tid & 31) == 0) {
+      red[tid >> 5] = mk;
+      queue[tid >> 5] = mv;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      mk = 0;
+      mv = 0;
+      for (int w = 0; w < kFusedThreads / 32; ++w) {
+        mk = max(mk, red[w]);
+        mv = max(mv, queue[w]);
+      }
+      s_am[0] = mk;
+      s_am[1] = mv;
+    }
+    __syncthreads();
+  }
+  QTRACE(2);
+  for (int t = 0; t < 2; ++t) {
+    const uint8_t* s = STAGED ? sm + t * slice : (const uint8_t*)p.x[t] + u0 * kUB;
+    const uint32_t abits = s_am[t];
+    if (abits >= 0x7F800000u) {  // non-finite tensor: leave the chunk undefined, report
+      if (tid == 0 && c == 0) atomicCAS(&p.status->code, 0, -6);
+      for (int i = tid; i < nu * 16; i += kFusedThreads) {  // first offending element of this slice
+        const uint32_t bits = DT == DT_BF16 ? ((uint32_t)reinterpret_cast<const uint16_t*>(s)[i] & 0x7FFFu) << 16
+                                            : reinterpret_cast<const uint32_t*>(s)[i] & 0x7FFFFFFFu;
+        if (bits >= 0x7F800000u) atomicMin(&p.status->first_bad, (unsigned long long)(t * NU * 16 + u0 * 16 + i));
+      }
+      continue;
+    }
+    const float amax = __uint_as_float(abits);
+    const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
+    const float rg = rcp_approx(g);
+    if (c == 0 && tid == 0) p.g_out[t] = g;
+    uint8_t* codes = p.codes[t];
+    uint8_t* scales = p.scales[t];
+    // two blocks per thread per iteration (independent streams for latency hiding)
+    for (int i = tid; i < nu; i += kQNB * kFusedThreads) {
+      int ib[kQNB];
+#pragma unroll
+      for (int b = 0; b < kQNB; ++b) ib[b] = i + b * kFusedThreads < nu ? i + b * kFusedThreads : i;
+      float v[kQNB][16];
+#pragma unroll
+      for (int b = 0; b < kQNB; ++b) {
+        const uint8_t* src = s + (size_t)ib[b] * kUB;
+        if (DT == DT_BF16) {
+          const uint4 x0 = *reinterpret_cast<const uint4*>(src), x1 = *reinterpret_cast<const uint4*>(src + 16);
+          const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[b][2 * k] = __uint_as_float(w[k] << 16);
+            v[b][2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 x = reinterpret_cast<const float4*>(src)[k];
+            v[b][4 * k] = x.x; v[b][4 * k + 1] = x.y; v[b][4 * k + 2] = x.z; v[b][4 * k + 3] = x.w;
+          }
+        }
+      }
+      uint32_t sb[kQNB], w0[kQNB], w1[kQNB];
+      const uint32_t flags = quantize_blocks_fast<kQNB>(v, g, rg, sb, w0, w1);
+#pragma unroll
+      for (int b = 0; b < kQNB; ++b) {
+        if (b > 0 && ib[b] == ib[0]) break;
+        if (flags & (1u << b)) queue[atomicAdd(&s_nq, 1)] = (uint32_t)ib[b];  // exact recompute below
+        const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
+        const uint32_t row = u / kNB;
+        const int j = (int)(u - row * kNB);
+        const uint32_t t_tok = row / (uint32_t)p.H;
+        const uint32_t h = row - t_tok * (uint32_t)p.H;
+        const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
+        *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(w0[b], w1[b]);
+        scales[orow * kNB + j] = (uint8_t)sb[b];
+      }
+    }
+    __syncthreads();
+    if (t == 0) QTRACE(4);
+    // deferred exact path for the flagged blocks (a few % of blocks; one thread per block)
+    const int nq = s_nq;
+    for (int e = tid; e < nq; e += kFusedThreads) {
+      const int ibk = (int)queue[e];
+      float v[16];
+      const uint8_t* src = s + (size_t)ibk * kUB;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        v[k] = DT == DT_BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
+                             : reinterpret_cast<const float*>(src)[k];
+      uint32_t sbe, a, bb;
+      quantize_block16_exact(v, g, sbe, a, bb);
+      const uint32_t u = (uint32_t)u0 + (uint32_t)ibk;
+      const uint32_t row = u / kNB;
+      const int j = (int)(u - row * kNB);
+      const uint32_t t_tok = row / (uint32_t)p.H;
+      const uint32_t h = row - t_tok * (uint32_t)p.H;
+      const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
+      *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(a, bb);
+      scales[orow * kNB + j] = (uint8_t)sbe;
+    }
+    __syncthreads();
+    if (tid == 0) s_nq = 0;
+    QTRACE(3 + 4 * t);
+  }
+}
+#undef QTRACE
+
 // Eq. 2: x^ = dec(c) dec(s) g.  dec(c) dec(s) is exact in fp32 (<= 7 significant
 // bits), so one __fmul_rn by g gives RN32 of the exact product.
 template <int D>
-__global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
+__global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DequantParams p) {
   constexpr int kNB = D / 16;
   const int tsr = blockIdx.y;
   const float g = p.g[tsr];
@@ -241,7 +602,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) export_kernel(const ExportParams p) {
+__global__ void __launch_bounds__(256) export_kernel(const __grid_constant__ ExportParams p) {
   constexpr int kNB = D / 16;
   const int tsr = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.g_out[tsr] = p.g[tsr];
@@ -266,7 +627,7 @@ struct WinSegs {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256) dequant_window_kernel(const DequantParams p, const float* gtab,
+__global__ void __launch_bounds__(256) dequant_window_kernel(const __grid_constant__ DequantParams p, const float* gtab,
                                                              const WinSegs ws) {
   constexpr int kNB = D / 16;
   const int tsr = blockIdx.y;
@@ -348,6 +709,66 @@ cudaError_t launch_quantize(const QuantParams& p, cudaStream_t st) {
     else quant_kernel<DT_FP32, 64><<<grid, 256, 0, st>>>(p);
   }
   return cudaGetLastError();
+}
+
+template <int DT, int D>
+cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,
+                           cudaStream_t st) {
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
+  const int64_t NU = (int64_t)p.rows * (D / 16);
+  int upc = (int)((NU + sms - 1) / sms);
+  if (upc < 64) upc = 64;
+  upc = (upc + 7) & ~7;  // 128-byte aligned V slice
+  const int G = (int)((NU + upc - 1) / upc);
+  const size_t smem = (size_t)2 * upc * kUB + (size_t)upc * sizeof(uint32_t);  // K, V slices + flag queue
+  if (smem > 220 * 1024 || G > kNumPartials) return cudaErrorNotSupported;
+  auto kern = quant_fused_kernel<DT, D, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the grid barrier is safe
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  (void)partials;
+  // counters -> the barrier slots: [G][2] x u64 (tag << 32 | amax bits) for K and V
+  return cudaLaunchKernelEx(&cfg, kern, p, counters, upc);
+}
+
+// second pass of the two-launch path (after launch_amax): per-block work as in the single-pass kernel
+template <int DT, int D>
+cudaError_t launch_quant2_t(const QuantParams& p, int sms, cudaStream_t st) {
+  const int64_t NU = (int64_t)p.rows * (D / 16);
+  int64_t G = sms;
+  if ((NU + G - 1) / G > 8192) G = (NU + 8191) / 8192;  // flag queue <= 32 KB of smem
+  const int upc = (int)((NU + G - 1) / G);
+  G = (NU + upc - 1) / upc;
+  const size_t smem = (size_t)upc * sizeof(uint32_t);
+  auto kern = quant_fused_kernel<DT, D, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)G, kFusedThreads, smem, st>>>(p, nullptr, upc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize2(const QuantParams& p, int sms, cudaStream_t st) {
+  if (p.dtype == DT_BF16)
+    return p.d == 128 ? launch_quant2_t<DT_BF16, 128>(p, sms, st) : launch_quant2_t<DT_BF16, 64>(p, sms, st);
+  return p.d == 128 ? launch_quant2_t<DT_FP32, 128>(p, sms, st) : launch_quant2_t<DT_FP32, 64>(p, sms, st);
+}
+
+cudaError_t launch_quantize_fused(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,
+                                  cudaStream_t st) {
+  if (p.dtype == DT_BF16)
+    return p.d == 128 ? launch_fused_t<DT_BF16, 128>(p, counters, partials, sms, st)
+                      : launch_fused_t<DT_BF16, 64>(p, counters, partials, sms, st);
+  return p.d == 128 ? launch_fused_t<DT_FP32, 128>(p, counters, partials, sms, st)
+                    : launch_fused_t<DT_FP32, 64>(p, counters, partials, sms, st);
 }
 
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t st) {

@@ -87,6 +87,7 @@ _SIGS = {
                                             ctypes.c_int32, _P, _P]),
     "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
     "kvq_debug_set_trace": (ctypes.c_int, [_P]),
+    "kvq_debug_force_two_pass": (ctypes.c_int, [_P, ctypes.c_int32]),
 }
 
 
@@ -167,6 +168,10 @@ class KVCache:
 
     def reset(self):
         _check(lib().kvq_cache_reset(self._h, _stream()), "kvq_cache_reset")
+
+    def force_two_pass(self, on=True):
+        """Debug: route appends through the amax + quantize two-launch path."""
+        _check(lib().kvq_debug_force_two_pass(self._h, 1 if on else 0), "kvq_debug_force_two_pass")
 
     def set_shot(self, start_frame, len_frames):
         _check(lib().kvq_set_shot(self._h, start_frame, len_frames), "kvq_set_shot")

@@ -96,6 +96,37 @@ def test_quantize_wan_shape_bitexact(variant, scale):
     assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
 
 
+@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_quantize_single_and_two_pass_bitexact(two_pass, dtype):
+    # the cooperative single-pass kernel and the amax + quantize two-launch path give the oracle's bytes
+    _gpu()
+    T, H, d = 4680, 12, 128
+    c = _cache(H, d, 1560, 3)
+    c.force_two_pass(two_pass)
+    _, k, v = synth.make_qkv(T, H, d, dtype, 1, 2)
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
+
+
+def test_quantize_lattice_inputs_take_exact_path():
+    # inputs on the NVFP4 lattice make every quotient an exact E2M1 value (the fast-divide guard fires
+    # for most blocks); codes must still be bit-exact, and re-quantizing the dequantized chunk is the
+    # identity (idempotence)
+    _gpu()
+    T, H, d = 256, 4, 128
+    c = _cache(H, d, 256, 1)
+    _, k, v = synth.make_qkv(T, H, d, "bf16", 0, 3)
+    c.append(0, 0, k.torch(DEV), v.torch(DEV))
+    K32, V32 = c.dequantize(0, 0, torch.float32)
+    c.append(0, 0, K32.contiguous(), V32.contiguous())      # overwrite with the lattice values
+    qk = nvfp4.quantize_kv_chunk(K32.cpu().numpy().astype(np.float64))
+    qv = nvfp4.quantize_kv_chunk(V32.cpu().numpy().astype(np.float64))
+    assert_chunk_bytes_equal(c.export(0, 0), qk, qv)
+    ref = nvfp4.quantize_kv_chunk(k.f64)
+    assert np.array_equal(qk["codes"], ref["codes"]) and np.array_equal(qk["scales"], ref["scales"])
+
+
 def test_quantize_edge_blocks_bitexact():
     # zero tensor (g = 1), zero blocks, underflow-promoted scales, -0.0, ragged T_c (not a multiple of 128)
     _gpu()

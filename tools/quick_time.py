@@ -27,3 +27,26 @@ flops = 4 * T * 32760 * d * H
 print(f"attention: {ta:.1f} us  {flops/ta/1e6:.1f} TFLOP/s  {T/ta*1e6/1e6:.3f} M q-tok/s")
 tq = timeit(lambda: c.append(0, 6, qs[6][1], qs[6][2]), 50)
 print(f"append: {tq:.2f} us  {T*H*d*2*(2+9/16)/tq/1e3:.1f} GB/s")
+# device time of the append alone: 20 appends captured in one CUDA graph (removes host launch cost)
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    c.append(0, 6, qs[6][1], qs[6][2])
+torch.cuda.current_stream().wait_stream(s)
+with torch.cuda.graph(g):
+    for _ in range(20):
+        c.append(0, 6, qs[6][1], qs[6][2])
+tg = timeit(lambda: g.replay(), 10) / 20
+print(f"append (graph): {tg:.2f} us  {T*H*d*2*(2+9/16)/tg/1e3:.1f} GB/s")
+c.force_two_pass(True)
+g2 = torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    c.append(0, 6, qs[6][1], qs[6][2])
+torch.cuda.current_stream().wait_stream(s)
+with torch.cuda.graph(g2):
+    for _ in range(20):
+        c.append(0, 6, qs[6][1], qs[6][2])
+tg2 = timeit(lambda: g2.replay(), 10) / 20
+print(f"append two-pass (graph): {tg2:.2f} us  {T*H*d*2*(2+9/16)/tg2/1e3:.1f} GB/s")
+c.force_two_pass(False)
