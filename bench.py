@@ -55,51 +55,49 @@ def n_keys():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled every 5 ms through NVML (the same counters
+    nvidia-smi's clocks.sm / clocks_event_reasons.* report) while the timed region runs."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                          pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for _, bits in self.rows for n, b in self.REASONS.items() if bits & b})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.max_mhz), "sm_min_mhz": float(min(sm)),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 5 ms"}
 
 
 def cpu_cores():
@@ -263,33 +261,62 @@ def run_gpu(args):
     flops = 4.0 * T_C * nk * D * H
     out = {"metric": METRIC, "value": value, "unit": "query-tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "nvfp4 KV (e2m1/e4m3/fp32 "
-           "scales), fp16 tensor-core MMA with fp32 accumulate, bf16 Q/K/V/O",
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "fp16",
+           "dtype_detail": "NVFP4 KV cache (e2m1 codes, e4m3 block scales, fp32 tensor scales); tensor-core "
+           "MMA in fp16 with fp32 accumulate; bf16 Q/K/V in, bf16 O out",
            "data": "synthetic (seeded SplitMix64 -> Box-Muller N(0,1) -> bf16; no weights needed)",
            "config": {"workload": WORKLOAD, "heads": H, "head_dim": D, "T_c": T_C, "tokens_per_frame": TPF,
                       "frames_per_chunk": T_FRAMES, "sink_frames": SINK, "window_frames": WINDOW,
                       "n_keys": nk, "chunk_index": CHUNK, "parallelism": f"ulysses-heads{world}" if world > 1 else "1 GPU",
                       "l2": "flushed (256 MiB write) before every timed step"},
-           "gpu_launches": args.steps * (3 if world == 1 else 6)}
+           # per step: N=1 quantize/append (1) + attention (1) + split-KV combine (1);
+           # N>1 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted)
+           "gpu_launches": args.steps * (3 if world == 1 else 7)}
     if uly is None:
         att_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_att]))
-        app_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
+        app_ms_ev = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
+        # the append alone is ~20 us: time it as 20 appends captured in one CUDA graph (removes the
+        # host launch cost an event pair around one python call would include); L2 is flushed first
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(st)
+        with torch.cuda.stream(side):
+            cache.append(0, CHUNK, k6, v6)
+        st.wait_stream(side)
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                cache.append(0, CHUNK, k6, v6)
+        gs = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            gs.append(e0.elapsed_time(e1) / 20)
+        app_ms = float(np.median(gs))
         ach = flops / (att_ms * 1e-3) / 1e12
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get("attn_kernel")
+                tj = json.load(f)
+                traffic = tj.get("attn_ws_kernel", {}).get("bytes")
+                traffic_app = tj.get("quant_fused_kernel", {}).get("bytes")
         except Exception:
-            pass
-        out["roofline"] = {"bound": "tensor", "kernel": "attn_kernel (fused dequant + QK^T + softmax + PV)",
-                           "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus,
-                           "traffic": traffic, "peak_source": f"{src} bf16_tflops_sustained (fp16 kind::f16 = same rate)",
-                           "frac_of_burst": ach / tf_burst, "ms": att_ms, "flops_per_launch": flops}
+            traffic_app = None
+        out["roofline"] = {"bound": "tensor", "kernel": "attn_ws_kernel + combine_kernel (fused dequant, QK^T, "
+                           "online softmax, PV on tcgen05)", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s",
+                           "frac": ach / tf_sus, "traffic": traffic,
+                           "peak_source": f"{src} bf16_tflops_sustained (fp16 kind::f16 runs at the bf16 rate)",
+                           "frac_of_burst": ach / tf_burst, "ms": att_ms, "flops_per_launch": flops,
+                           "algorithmic_flops": "4 * T_c * |K_eff| * d * H"}
         app_bytes = T_C * H * D * 2 * (2 + 9 / 16)
-        out["roofline_append"] = {"bound": "hbm", "kernel": "amax_kernel + quant_kernel",
+        out["roofline_append"] = {"bound": "hbm", "kernel": "quant_fused_kernel (single-pass quantize/append)",
                                   "achieved": app_bytes / (app_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                   "frac": app_bytes / (app_ms * 1e-3) / 1e9 / hbm, "us": app_ms * 1e3,
-                                  "algorithmic_bytes": app_bytes}
+                                  "us_event_single_call": app_ms_ev * 1e3, "traffic": traffic_app,
+                                  "algorithmic_bytes": app_bytes, "timing": "CUDA graph of 20 appends, L2 flushed"}
         out["kv_stream_gbs"] = 2 * nk * H * D * 9 / 16 / (att_ms * 1e-3) / 1e9
         out["attention_tflops"] = ach
         out["e2e"] = e2e
@@ -336,7 +363,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")

@@ -571,35 +571,38 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 }
 
 // Merge the partial pieces of every split unit: O = sum_p 2^(m_p - m) O_p / sum_p 2^(m_p - m) l_p,
-// pieces in increasing CTA order (deterministic).  One thread per (unit row, 4 output columns).
+// pieces in increasing CTA order (deterministic).  A unit is split exactly when a CTA range boundary
+// falls strictly inside it; CTA b of this kernel handles the boundary of attention CTA b (if it is
+// the first boundary inside its unit), so only split units are touched.  Thread = (row, 4 columns).
 template <int D>
-__global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ AttnParams p, int n) {
+__global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ AttnParams p, int n) {
   const int64_t W = (int64_t)p.units * n;
   const int G = p.grid;
-  const int tpr = D / 4;  // threads per row
-  const int64_t total = (int64_t)p.units * 256 * tpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int unit = (int)(i / (256 * tpr));
-    const int rr = (int)((i / tpr) % 256);
-    const int c4 = (int)(i % tpr);
-    const int h = unit / p.qpairs, q0 = (unit - h * p.qpairs) * 256;
+  const int b = blockIdx.x + 1;  // boundary between attention CTAs b-1 and b
+  const int64_t sb = range_begin(b, W, G);
+  if (sb % n == 0) return;                                   // boundary on a unit edge: no split
+  const int unit = (int)(sb / n);
+  const int64_t s0 = (int64_t)unit * n, s1 = s0 + n;
+  if (range_begin(b - 1, W, G) > s0) return;                 // an earlier boundary owns this unit
+  const int c0 = b - 1;                                      // CTA holding the unit's first piece
+  const bool c0_first = range_begin(c0, W, G) == s0;         // ... as its first piece?
+  int c1 = b;
+  while (c1 + 1 < G && range_begin(c1 + 1, W, G) < s1) ++c1;  // last CTA with a piece of the unit
+  const int h = unit / p.qpairs, q0 = (unit - h * p.qpairs) * 256;
+  constexpr int kTpr = D / 4;  // threads per row
+  for (int i = threadIdx.x; i < 256 * kTpr; i += blockDim.x) {
+    const int rr = i / kTpr, c4 = i - rr * kTpr;
     const int t = q0 + rr;
     if (t >= p.Tq) continue;
-    const int64_t s0 = (int64_t)unit * n, s1 = s0 + n;
-    // CTA owning step s0: largest c with range_begin(c) <= s0
-    int c0 = (int)((s0 * G) / W);
-    while (c0 + 1 < G && range_begin(c0 + 1, W, G) <= s0) ++c0;
-    while (c0 > 0 && range_begin(c0, W, G) > s0) --c0;
-    if (range_begin(c0, W, G) <= s0 && range_begin(c0 + 1, W, G) >= s1) continue;  // unsplit: written directly
     float m = -INFINITY;
-    for (int cc = c0; cc < G && range_begin(cc, W, G) < s1; ++cc) {
-      const int slot = range_begin(cc, W, G) >= s0 ? 2 * cc : 2 * cc + 1;
+    for (int cc = c0; cc <= c1; ++cc) {
+      const int slot = (cc == c0 && !c0_first) ? 2 * cc + 1 : 2 * cc;  // first piece = c0's last; others = their first
       m = fmaxf(m, p.ws[(size_t)slot * p.ws_slot_floats + 256 * D + rr]);
     }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float l = 0.0f;
-    for (int cc = c0; cc < G && range_begin(cc, W, G) < s1; ++cc) {
-      const int slot = range_begin(cc, W, G) >= s0 ? 2 * cc : 2 * cc + 1;
+    for (int cc = c0; cc <= c1; ++cc) {
+      const int slot = (cc == c0 && !c0_first) ? 2 * cc + 1 : 2 * cc;
       const float* base = p.ws + (size_t)slot * p.ws_slot_floats;
       const float w = exp2f(base[256 * D + rr] - m);
       l += w * base[256 * D + 256 + rr];
@@ -643,9 +646,7 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   kern<<<G, kThreads, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess || !split) return e;
-  const int64_t work = (int64_t)p.units * 256 * (D / 4);
-  const int cgrid = (int)((work + 255) / 256 < 148 * 8 ? (work + 255) / 256 : 148 * 8);
-  combine_kernel<D><<<cgrid, 256, 0, st>>>(p, n);
+  if (G > 1) combine_kernel<D><<<G - 1, 512, 0, st>>>(p, n);  // one CTA per range boundary
   return cudaGetLastError();
 }
 

@@ -1,0 +1,68 @@
+"""Summarise ncu captures of a round into profiles/ (run here, on the CPU box, after gpurun).
+usage: python tools/summarize_ncu.py <tag>"""
+import csv, io, json, os, subprocess, sys
+from collections import defaultdict
+
+tag = sys.argv[1]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = os.path.join(ROOT, "gpurun_out")
+P = os.path.join(ROOT, "profiles")
+os.makedirs(P, exist_ok=True)
+out = [f"# ncu summary, round tag {tag}\n"]
+
+# launch list (cold-cache, serialised: compare shares, not absolutes)
+rows = list(csv.reader(open(os.path.join(G, f"launches_{tag}.csv"))))
+hdr = None
+tot = defaultdict(float)
+cnt = defaultdict(int)
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").strip()
+        v = float(d["Metric Value"])
+        unit = d.get("Metric Unit", "ns")
+        v = v / 1000.0 if unit == "ns" else v * (1000.0 if unit == "ms" else 1.0)
+        tot[name] += v
+        cnt[name] += 1
+ours = {k: v for k, v in tot.items() if "kvq" in k or "attn" in k or "quant" in k or "combine" in k}
+s = sum(ours.values())
+out.append("## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, bench.py --steps 3 --warmup 3)\n")
+out.append("| kernel | launches | total us | mean us | share of our kernels |\n|---|---|---|---|---|\n")
+for k, v in sorted(ours.items(), key=lambda kv: -kv[1]):
+    out.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {v / cnt[k]:.2f} | {100 * v / s:.1f}% |\n")
+
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__issue_active.avg.pct_of_peak_sustained_elapsed", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "sm__cycles_elapsed.avg.per_second", "smsp__inst_executed.sum"]
+traffic = {}
+for rep, label in ((f"attn_{tag}", "attn_ws_kernel"), (f"quant_{tag}", "quant_fused_kernel")):
+    path = os.path.join(G, rep + ".ncu-rep")
+    if not os.path.exists(path):
+        continue
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, units = r[0], r[1]
+    for row in r[2:]:
+        d = dict(zip(h, row))
+        u = dict(zip(h, units))
+        out.append(f"\n## `{d['Kernel Name'][:90]}` (`ncu --set full`, one launch)\n\n| metric | value |\n|---|---|\n")
+        for k in keys:
+            if k in d:
+                out.append(f"| {k} | {d[k]} {u.get(k, '')} |\n")
+        def mb(k):
+            v = float(d[k]); un = u.get(k, "")
+            return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(un, 1.0)
+        traffic[label] = {"dram_read_MB": mb("dram__bytes_read.sum"), "dram_write_MB": mb("dram__bytes_write.sum"),
+                          "bytes": (mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")) * 1e6, "source": rep}
+open(os.path.join(P, f"ncu_summary_{tag}.md"), "w").write("".join(out))
+json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+os.system(f"cp {os.path.join(G, f'launches_{tag}.csv')} {os.path.join(P, f'launches_{tag}.csv')}")
+print("".join(out))
