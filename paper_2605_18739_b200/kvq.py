@@ -281,6 +281,38 @@ def ulysses_qkv_bytes(Ts, H, d, P, dst, dtype=torch.bfloat16):
     return int(lib().kvq_ulysses_qkv_bytes(Ts, H, d, P, dst, _out_code(dtype)))
 
 
+def ulysses_pack(Q, K, V, P, send=None, scratch=None):
+    """kvq_ulysses_pack_qkv: this rank's shards [Ts, H, d] -> the all-to-allv send buffer (u8)."""
+    Ts, H, d = Q.shape
+    sizes = [ulysses_qkv_bytes(Ts, H, d, P, p, Q.dtype) for p in range(P)]
+    if send is None:
+        send = torch.empty(sum(sizes), dtype=torch.uint8, device=Q.device)
+    if scratch is None:
+        scratch = torch.empty(8192, dtype=torch.uint8, device=Q.device)
+    _check(lib().kvq_ulysses_pack_qkv(_ptr(Q), _ptr(K), _ptr(V), _dt(Q), Ts, H, d, P, _ptr(send), _ptr(scratch),
+                                      _stream()), "kvq_ulysses_pack_qkv")
+    return send, sizes
+
+
+def ulysses_unpack_qkv(recv, Ts, Hr, d, P, dtype=torch.bfloat16):
+    """kvq_ulysses_unpack_qkv: P received segments -> Q, K, V [P*Ts, Hr, d] + global amax (K, V)."""
+    Q = torch.empty((P * Ts, Hr, d), dtype=dtype, device=recv.device)
+    K, V = torch.empty_like(Q), torch.empty_like(Q)
+    amax = torch.empty(2, dtype=torch.float32, device=recv.device)
+    _check(lib().kvq_ulysses_unpack_qkv(_ptr(recv), _out_code(dtype), Ts, Hr, d, P, _ptr(Q), _ptr(K), _ptr(V),
+                                        _ptr(amax), _stream()), "kvq_ulysses_unpack_qkv")
+    return Q, K, V, amax
+
+
+def ulysses_unpack_o(recv, Ts, H, d, P, dtype=torch.bfloat16, out=None):
+    """kvq_ulysses_unpack_o: P received O token blocks [Ts, H_p, d] -> this rank's O shard [Ts, H, d]."""
+    if out is None:
+        out = torch.empty((Ts, H, d), dtype=dtype, device=recv.device)
+    _check(lib().kvq_ulysses_unpack_o(_ptr(recv), _out_code(dtype), Ts, H, d, P, _ptr(out), _stream()),
+           "kvq_ulysses_unpack_o")
+    return out
+
+
 class Ulysses:
     """Head-sharded chunk step of one rank (App. C; App. D).
 

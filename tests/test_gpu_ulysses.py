@@ -1,0 +1,91 @@
+"""Head-sharded (Ulysses) path on one GPU, with the all-to-all simulated by byte slicing (-m gpu).
+
+Every rank's compute runs the library kernels (pack, unpack, quantize/append with the
+piggybacked global amax, attention, O unpack); only the collective is replaced by the exact byte
+movement NCCL's all_to_all_single performs.  Checks (readings Z2/Z18): each rank's cache bytes equal
+the 1-GPU cache's bytes for its heads bit-exactly, and the reassembled O matches the oracle within
+the fp32 tolerance and the 1-GPU result closely.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import nvfp4
+from oracle.cache import OracleKVCache
+from paper_2605_18739_b200 import kvq, synth
+
+from gpu_util import check_fp32_out
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _a2a(sends, send_sizes, recv_sizes):
+    """all_to_all_single semantics: rank p receives, in source order, source r's p-th segment."""
+    P = len(sends)
+    offs = [np.concatenate([[0], np.cumsum(s)]) for s in send_sizes]
+    return [torch.cat([sends[r][int(offs[r][p]):int(offs[r][p]) + send_sizes[r][p]] for r in range(P)])
+            for p in range(P)]
+
+
+@pytest.mark.parametrize("P,H", [(2, 12), (4, 12), (8, 12), (8, 24), (3, 7)])
+def test_ulysses_simulated_matches_single_gpu(P, H):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d = 40, 3, 128
+    T = tpf * fc                       # 120 tokens per chunk, divisible by P for P in {2,3,4,8}
+    Ts = T // P
+    sink, window = 3, 9
+    parts = [kvq.head_partition(H, P, r) for r in range(P)]
+    caches = [kvq.KVCache(1, h1 - h0, d, tpf, fc, sink_frames=sink, window_frames=window, max_chunk_slots=8,
+                          device=DEV) for h0, h1 in parts]
+    ref = kvq.KVCache(1, H, d, tpf, fc, sink_frames=sink, window_frames=window, max_chunk_slots=8, device=DEV)
+    orc = OracleKVCache(1, H, d, tpf, fc)
+    for ch in range(5):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch)
+        Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+        mask = kvq.Mask(ch, sink, window)
+        # ---- 1 GPU reference
+        ref.append(0, ch, K, V)
+        O_ref = ref.attention(0, Q, mask, torch.float32)
+        orc.append(0, ch, k.f64, v.f64)
+        # ---- P ranks: pack -> all-to-all -> unpack -> append (global amax) -> attention -> a2a -> unpack
+        packed = [kvq.ulysses_pack(Q[r * Ts:(r + 1) * Ts].contiguous(), K[r * Ts:(r + 1) * Ts].contiguous(),
+                                   V[r * Ts:(r + 1) * Ts].contiguous(), P) for r in range(P)]
+        recv = _a2a([s for s, _ in packed], [sz for _, sz in packed], None)
+        O_locals = []
+        for p, (h0, h1) in enumerate(parts):
+            Hr = h1 - h0
+            Ql, Kl, Vl, amax = kvq.ulysses_unpack_qkv(recv[p], Ts, Hr, d, P)
+            assert torch.equal(Ql, Q[:, h0:h1]) and torch.equal(Kl, K[:, h0:h1]) and torch.equal(Vl, V[:, h0:h1])
+            caches[p].append(0, ch, Kl, Vl, amax_kv=amax)
+            O_locals.append(caches[p].attention(0, Ql, mask, torch.float32))
+        # O return: rank p sends token block r of its O_local to rank r (equal splits)
+        o_bytes = [[Ts * (h1 - h0) * d * 4 for _ in range(P)] for h0, h1 in parts]
+        o_recv = _a2a([o.view(torch.uint8).reshape(-1) for o in O_locals], o_bytes, None)
+        O_full = torch.cat([kvq.ulysses_unpack_o(o_recv[r], Ts, H, d, P, torch.float32) for r in range(P)])
+        # ---- codes bit-exact per head (Z18), O close to 1 GPU and within tolerance of the oracle
+        ex = ref.export(0, ch)
+        for p, (h0, h1) in enumerate(parts):
+            e = caches[p].export(0, ch)
+            for name in ("codes_k", "scales_k", "codes_v", "scales_v"):
+                full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
+                assert torch.equal(e[name], full), (p, name)
+            assert torch.equal(e["g_k"], ex["g_k"]) and torch.equal(e["g_v"], ex["g_v"])
+        # not bit-identical: the stream-K split points differ, and a split piece rounds P to fp16
+        # against its own running max
+        assert torch.allclose(O_full, O_ref, rtol=1e-3, atol=2e-4)
+        check_fp32_out(O_full.cpu().numpy(), orc.attend(0, ch, q.f64, sink, window))
+
+
+def test_pack_trailer_carries_shard_amax():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    Ts, H, d, P = 16, 12, 64, 4
+    Q, K, V = (synth.make_tensor((Ts, H, d), "bf16", seed=s).torch(DEV) for s in (1, 2, 3))
+    send, sizes = kvq.ulysses_pack(Q, K, V, P)
+    off = 0
+    for p, sz in enumerate(sizes):
+        tr = send[off + sz - 16: off + sz].view(torch.float32)
+        assert tr[0].item() == K.float().abs().max().item() and tr[1].item() == V.float().abs().max().item()
+        off += sz
