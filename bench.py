@@ -232,30 +232,41 @@ def run_gpu(args):
     value = T_C / (step_ms * 1e-3)
 
     # ---- end-to-end through the public API with host buffers (pinned), copies inside the region
-    e2e = None
-    if uly is None:
-        hq, hk, hv = (x.pin_memory() for x in chunks[CHUNK])
-        hO = torch.empty((T_C, H, D), dtype=torch.bfloat16).pin_memory()
-        gq, gk, gv = (torch.empty_like(x, device=dev) for x in (hq, hk, hv))
-        for _ in range(2):
-            gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
+    # (each rank copies its own shard in and its O shard out; at N=1 the shard is the whole chunk)
+    hq, hk, hv = (x.pin_memory() for x in chunks[CHUNK])
+    hO = torch.empty((Ts, H, D), dtype=torch.bfloat16).pin_memory()
+    gq, gk, gv = (torch.empty_like(x, device=dev) for x in (hq, hk, hv))
+
+    def e2e_step():
+        gq.copy_(hq, non_blocking=True)
+        gk.copy_(hk, non_blocking=True)
+        gv.copy_(hv, non_blocking=True)
+        if uly is None:
             cache.append(0, CHUNK, gk, gv)
             cache.attention(0, gq, mask, out=O)
-            hO.copy_(O, non_blocking=True)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(args.steps):
-            gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
-            cache.append(0, CHUNK, gk, gv)
-            cache.attention(0, gq, mask, out=O)
-            hO.copy_(O, non_blocking=True)
-        e1.record(st)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.steps
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
-        e2e = {"value": T_C / (e2e_ms * 1e-3), "unit": "query-tokens/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hO.numel() * 2)}
+        else:
+            uly.step(0, CHUNK, gq, gk, gv, mask, out=O)
+        hO.copy_(O, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv)) * world
+    e2e = {"value": T_C / (e2e_ms * 1e-3), "unit": "query-tokens/s", "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hO.numel() * 2 * world),
+           "note": "bytes summed over ranks; pinned host buffers, copies inside the timed region"}
 
     hbm, tf_burst, tf_sus, src = peaks()
     flops = 4.0 * T_C * nk * D * H
@@ -319,7 +330,15 @@ def run_gpu(args):
                                   "algorithmic_bytes": app_bytes, "timing": "CUDA graph of 20 appends, L2 flushed"}
         out["kv_stream_gbs"] = 2 * nk * H * D * 9 / 16 / (att_ms * 1e-3) / 1e9
         out["attention_tflops"] = ach
-        out["e2e"] = e2e
+    else:
+        # multi-GPU: the whole distributed layer step against the tensor roofline of all N GPUs
+        ach = flops / (step_ms * 1e-3) / 1e12
+        out["roofline"] = {"bound": "tensor", "kernel": "whole head-sharded layer step (pack, NCCL all-to-all, "
+                           "append, attention, all-to-all, unpack), max over ranks", "achieved": ach,
+                           "peak": tf_sus * world, "unit": "TFLOP/s", "frac": ach / (tf_sus * world), "traffic": None,
+                           "peak_source": f"{src} bf16_tflops_sustained x {world} GPUs",
+                           "head_split": [kvq.head_partition(H, P, r) for r in range(P)]}
+    out["e2e"] = e2e
     out["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu:
         est, desc = oracle_sample()

@@ -33,3 +33,7 @@ print("WG1 softmax dur median", np.median(t[5:60, 5] - t[5:60, 4]), "wait1 media
 print("dequant K->V median", np.median(t[5:60, 7] - t[5:60, 6]), "dequant period", np.median(np.diff(t[5:60, 6])))
 print("PV0 issue after P0 done", np.median(t[5:60, 8] - t[5:60, 2]), "PV1 issue after P1 done", np.median(t[5:60, 10] - t[5:60, 5]))
 print("S0(g+1) ready after PV0(g) issue", np.median(t[6:61, 1] - t[5:60, 8]))
+s = t[5:60]
+print("WG0 softmax phases (median cycles): S-ready->LDTM done", np.median(s[:, 12] - s[:, 1]),
+      " max", np.median(s[:, 13] - s[:, 12]), " exp loop", np.median(s[:, 14] - s[:, 13]),
+      " P store+rescale", np.median(s[:, 15] - s[:, 14]), " ->arrive", np.median(s[:, 2] - s[:, 15]))
