@@ -40,9 +40,14 @@ constexpr int kRegSoftmax = 176, kRegDequant = 80, kRegMma = 80;
 // Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
 // FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
 #ifndef KVQ_POLY_PAIRS
-#define KVQ_POLY_PAIRS 1
+#define KVQ_POLY_PAIRS 2
 #endif
 constexpr int kPolyPairs = KVQ_POLY_PAIRS;
+// Lazy-rescale threshold in log2 units (0 = exact running max, O rescaled whenever it grows).
+#ifndef KVQ_LAZY_LOG2
+#define KVQ_LAZY_LOG2 4.0f
+#endif
+constexpr float kLazyLog2 = KVQ_LAZY_LOG2;
 
 template <int N>
 KVQ_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -332,11 +337,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           mx3 = fmax3(mx3, __uint_as_float(s[kk + 6]), __uint_as_float(s[kk + 7]));
         }
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        const float m_new = fmaxf(m_run, mx * cs);
+#ifdef KVQ_EXPERIMENT_NO_MAX  // timing experiments only (wrong results)
+        const float m_new = j > 0 ? m_run : mx * cs;
+#else
+        // Lazy max (FA4-style): the reference point moves only when the tile max exceeds it by more
+        // than kLazyLog2 (P <= 2^kLazyLog2, far inside fp16); otherwise O needs no rescale.  The row
+        // sum l is taken from the fp16-ROUNDED P (the weights the PV MMA actually uses), so the
+        // normalisation stays exactly consistent for peaked rows.
+        const float m_tile = mx * cs;
+        const float m_new = (j == 0 || m_tile > m_run + kLazyLog2) ? fmaxf(m_run, m_tile) : m_run;
+#endif
         const float alpha = ex2_approx(m_run - m_new);
-        // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp32 p (two packed chains)
+        // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp16-rounded p (two packed chains)
         const uint64_t cs2 = f32x2_pack(cs, cs), mneg2 = f32x2_pack(-m_new, -m_new);
         uint64_t acc0 = 0, acc1 = 0;
+        float la[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int kk = 0; kk < 64; ++kk) {
           const uint64_t x2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2, mneg2);
@@ -348,19 +363,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
             p0 = ex2_approx(x0);
             p1 = ex2_approx(x1);
           }
+          const uint32_t pk = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
+          s[kk] = pk;
+#if defined(KVQ_SUM_UNROUNDED)
           if (kk & 1) acc1 = fadd2(acc1, f32x2_pack(p0, p1));
           else acc0 = fadd2(acc0, f32x2_pack(p0, p1));
-          s[kk] = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
+#elif !defined(KVQ_EXPERIMENT_NO_SUM)
+          // mixed-precision adds (FHADD: fp32 += fp16 lane) of the rounded P, four chains
+          if (MMA_BF16) {
+            asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.bf16 %0, l, %0;\n add.rn.f32.bf16 %1, h, %1;\n}"
+                : "+f"(la[(kk & 1) * 2]), "+f"(la[(kk & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
+          } else {
+            asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.f16 %0, l, %0;\n add.rn.f32.f16 %1, h, %1;\n}"
+                : "+f"(la[(kk & 1) * 2]), "+f"(la[(kk & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
+          }
+#endif
         }
         float a0, a1, b0, b1;
         f32x2_unpack(acc0, a0, a1);
         f32x2_unpack(acc1, b0, b1);
-        l_run = l_run * alpha + ((a0 + a1) + (b0 + b1));
+        l_run = l_run * alpha + ((a0 + a1) + (b0 + b1)) + ((la[0] + la[1]) + (la[2] + la[3]));
         KVQ_TMEM_ST32(tS, s);
         KVQ_TMEM_ST32(tS + 32, (s + 32));
         // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
         // PV_i(j-1) is complete here (issued before QK_i(j), whose commit we waited on).
+#ifdef KVQ_EXPERIMENT_NO_RESCALE
+        if (false) {
+#else
         if (j > 0) {
+#endif
           const float f = alpha * (gv_run / gv);
           if (!__all_sync(0xffffffffu, f == 1.0f)) {
             // two 32-column chunks per TMEM round trip, staged in the free half of s[]
