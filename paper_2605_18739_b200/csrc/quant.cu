@@ -35,17 +35,20 @@ KVQ_DEV uint32_t warp_max_u32(uint32_t v) {
 }
 
 // |x| bit pattern of every lane of a 16-byte vector, max-reduced, as an fp32 bit pattern.
+KVQ_DEV uint32_t max_u16x2(uint32_t a, uint32_t b, uint32_t c) {  // VIMNMX3.U16x2
+  uint32_t r;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  asm("max.u16x2 %0, %0, %1;" : "+r"(r) : "r"(c));
+  return r;
+}
+
 template <int DT>
 KVQ_DEV uint32_t vec_absmax_bits(uint4 v) {
   if (DT == DT_BF16) {
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t m = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      m = max(m, (w[i] & 0x7FFFu) << 16);
-      m = max(m, w[i] & 0x7FFF0000u);
-    }
-    return m;
+    // |bf16| bit patterns compare like unsigned 16-bit integers: packed 2-lane max
+    const uint32_t m2 = max_u16x2(max_u16x2(v.x & 0x7FFF7FFFu, v.y & 0x7FFF7FFFu, v.z & 0x7FFF7FFFu),
+                                  v.w & 0x7FFF7FFFu, 0u);
+    return max((m2 & 0xFFFFu) << 16, m2 & 0xFFFF0000u);
   } else {
     return max(max(v.x & 0x7FFFFFFFu, v.y & 0x7FFFFFFFu), max(v.z & 0x7FFFFFFFu, v.w & 0x7FFFFFFFu));
   }
@@ -154,6 +157,14 @@ KVQ_DEV uint32_t e2m1x8(const float* q) {
 // the top two in {-2..5} mod 2^21) sends the whole block through exact __fdiv_rn.  The result is
 // bit-identical to the correctly rounded definition; the guard fires for ~4e-6 of random quotients
 // (and for exact lattice values / zeros, which simply take the slow path).
+// n / dv for n < 2^24 via a float reciprocal and one-step integer correction (exact)
+KVQ_DEV uint32_t div_small(uint32_t n, uint32_t dv, float inv) {
+  uint32_t q = (uint32_t)__float2int_rz((float)n * inv);
+  if (q * dv > n) --q;
+  if ((q + 1) * dv <= n) ++q;
+  return q;
+}
+
 KVQ_DEV float rcp_approx(float x) {
   float r;
   asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -319,6 +330,15 @@ KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
   uint32_t m = 0;
   const uint32_t base = smem_u32(s);  // explicit ld.shared (LDS.128), four vectors in flight
   int i = threadIdx.x * 16;
+  if (DT == DT_BF16) {  // accumulate packed |bf16| maxima (0.75 instr/element), convert once
+    uint32_t m2 = 0;
+    for (; i < nbytes; i += kFusedThreads * 16) {
+      const uint4 a = ld_shared_v4(base + i);
+      m2 = max_u16x2(m2, a.x & 0x7FFF7FFFu, a.y & 0x7FFF7FFFu);
+      m2 = max_u16x2(m2, a.z & 0x7FFF7FFFu, a.w & 0x7FFF7FFFu);
+    }
+    return max((m2 & 0xFFFFu) << 16, m2 & 0xFFFF0000u);
+  }
   for (; i + 3 * kFusedThreads * 16 < nbytes; i += 4 * kFusedThreads * 16) {
     const uint4 a = ld_shared_v4(base + i), b = ld_shared_v4(base + i + kFusedThreads * 16);
     const uint4 c = ld_shared_v4(base + i + 2 * kFusedThreads * 16), d = ld_shared_v4(base + i + 3 * kFusedThreads * 16);
@@ -484,6 +504,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     const float amax = __uint_as_float(abits);
     const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
     const float rg = rcp_approx(g);
+    const float invH = 1.0f / (float)p.H;
     if (c == 0 && tid == 0) p.g_out[t] = g;
     uint8_t* codes = p.codes[t];
     uint8_t* scales = p.scales[t];
@@ -521,7 +542,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
         const uint32_t row = u / kNB;
         const int j = (int)(u - row * kNB);
-        const uint32_t t_tok = row / (uint32_t)p.H;
+        const uint32_t t_tok = div_small(row, (uint32_t)p.H, invH);
         const uint32_t h = row - t_tok * (uint32_t)p.H;
         const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
         *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(w0[b], w1[b]);
