@@ -59,7 +59,7 @@ Layout make_layout(const kvq_config* c) {
   L.off_partials = off; off += align_up(2 * kNumPartials * sizeof(uint32_t), kAlign);
   L.off_status = off; off += align_up(sizeof(DevStatus), kAlign);
   L.off_counters = off;  // grid-barrier slots of the single-pass quantizer: [CTA][K|V] u64
-  off += align_up((size_t)2 * kNumPartials * sizeof(unsigned long long), kAlign);
+  off += align_up((size_t)kMaxFusedCtas * kSlotU64 * sizeof(unsigned long long), kAlign);
   L.off_ws = off; off += align_up(attn_ws_bytes(c->head_dim), kAlign);
   L.total = off;
   return L;

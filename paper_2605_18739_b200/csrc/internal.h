@@ -7,6 +7,8 @@ namespace kvq {
 
 constexpr int kTileKeys = 128;     // keys per attention tile; slots are padded to a multiple
 constexpr int kNumPartials = 592;  // amax partials per tensor (4 x 148 SMs)
+constexpr int kMaxFusedCtas = 192;   // single-pass quantizer grid limit
+constexpr int kSlotU64 = 16;        // one 128-byte line per barrier slot: [K, V, pad...] u64
 constexpr int kMaxSegs = 48;       // key segments per attention call
 
 enum DType : int { DT_BF16 = 0, DT_FP32 = 1, DT_FP16 = 2 };

@@ -146,17 +146,6 @@ KVQ_DEV uint32_t e2m1x8(const float* q) {
   return r;
 }
 
-// One 16-element block, definition R1 (reading Z4):
-//   s = E4M3_RNE_SAT(RN32(RN32(bmax / g) / 6)) (0 -> 2^-9; zero block -> 0x00, codes 0x00),
-//   d_b = RN32(dec(s) * g),  c = E2M1_RNE_SAT(RN32(x / d_b)).
-// The per-element quotient uses a per-block reciprocal r = RN32(1/d_b) and one FMA correction
-// (q0 = x r, e = x - q0 d_b exact, q1 = q0 + e r; packed fp32x2), which is within 1 ulp of
-// RN32(x/d_b).  The E2M1 code of q1 can then differ from the code of RN32(x/d_b) only if q1 lies
-// within 1 ulp of an E2M1 rounding midpoint (0.25, 0.75, ..., 5 -- all <= 3 significant bits), so
-// every quotient within [-2, +5] ulps of ANY value with <= 3 significant bits (mantissa bits below
-// the top two in {-2..5} mod 2^21) sends the whole block through exact __fdiv_rn.  The result is
-// bit-identical to the correctly rounded definition; the guard fires for ~4e-6 of random quotients
-// (and for exact lattice values / zeros, which simply take the slow path).
 // n / dv for n < 2^24 via a float reciprocal and one-step integer correction (exact)
 KVQ_DEV uint32_t div_small(uint32_t n, uint32_t dv, float inv) {
   uint32_t q = (uint32_t)__float2int_rz((float)n * inv);
@@ -165,26 +154,26 @@ KVQ_DEV uint32_t div_small(uint32_t n, uint32_t dv, float inv) {
   return q;
 }
 
-KVQ_DEV float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-// a / b within 1 ulp of RN32(a/b), given rb ~ 1/b (relative error <~ 2^-22): q0 = a*rb, then one
-// FMA residual correction.
-KVQ_DEV float div_corrected(float a, float b, float rb) {
+// RN32(a / b) given rb = RN32(1 / b) (Markstein's theorem; see quantize_blocks_fast).
+KVQ_DEV float div_markstein(float a, float b, float rb) {
   const float q0 = __fmul_rn(a, rb);
   return __fmaf_rn(__fmaf_rn(-q0, b, a), rb, q0);
 }
 
-// NB blocks at once (independent instruction streams for latency hiding).  The scale uses the
-// same idea as the codes: u1 ~ RN32(RN32(bmax/g)/6) is within 3 ulps of the exact value, and the
-// E4M3 rounding decision can only differ when u1 lies within 3 ulps of an E4M3 midpoint (<= 5
-// significant bits), detected from the 19 mantissa bits below the top four; such blocks recompute
-// t and u with __fdiv_rn.
-// Fast path for NB blocks; bit b of the return value is set when block b's scale or one of its
-// codes might differ from the exact definition -- the caller then recomputes that block with
-// quantize_block16_exact (deferred, so the rare exact path does not stall whole warps).
+// One 16-element block, definition R1 (reading Z4):
+//   s = E4M3_RNE_SAT(RN32(RN32(bmax / g) / 6)) (0 -> 2^-9; zero block -> 0x00, codes 0x00),
+//   d_b = RN32(dec(s) * g),  c = E2M1_RNE_SAT(RN32(x / d_b)).
+// Every quotient is computed without a divide by Markstein's correction: with y = RN32(1/b) (a
+// correctly rounded reciprocal) and q0 = RN32(a y) (within 1 ulp of a/b), the residual
+// e = a - q0 b is exact under FMA and RN32(q0 + e y) = RN32(a/b) exactly (Muller et al.,
+// Handbook of Floating-Point Arithmetic, Markstein's theorem; no overflow/underflow).  So the fast
+// path is bit-identical to the definition, not merely close: 1/g is rounded once per CTA, 1/6 is a
+// constant, 1/d_b is one rcp.rn per block, and each element costs one FMUL2 + two FFMA2 per pair.
+// The element quotients are formed negated (y' = -1/d_b): q0' = x y', e = fma(q0', d_b, x),
+// q1' = fma(e, y', q0') = -RN32(x/d_b) including the sign of zero (x = -0 gives q1' = +0), and the
+// E2M1 codes of the negation are flipped back with one XOR per 8 codes.  The theorem's range
+// conditions hold for 2^-60 <= g <= 2^60 (checked per tensor by the caller) and d_b >= 2^-64
+// (checked here: bit b of the return value sends block b through quantize_block16_exact).
 template <int NB>
 KVQ_DEV uint32_t quantize_blocks_fast(const float (&v)[NB][16], float g, float rg, uint32_t (&sbyte)[NB],
                                       uint32_t (&w0)[NB], uint32_t (&w1)[NB]) {
@@ -198,30 +187,28 @@ KVQ_DEV uint32_t quantize_blocks_fast(const float (&v)[NB][16], float g, float r
       m1 = fmax3(m1, fabsf(v[b][k + 2]), fabsf(v[b][k + 3]));
     }
     const float bmax = fmaxf(m0, m1);
-    const float u = div_corrected(div_corrected(bmax, g, rg), 6.0f, 0.16666667163372040f);
-    uint32_t mn = (__float_as_uint(u) + 4u) & 0x7FFF8u;  // 0 <=> u near an E4M3 midpoint
+    const float t = div_markstein(bmax, g, rg);
+    const float u = div_markstein(t, 6.0f, 0.16666667163372040f);  // RN32(1/6)
     uint32_t s = e4m3_from_f32(u);
     if (s == 0) s = 1;                          // SPEC.md:191 underflow promotion
     if (!(bmax > 0.0f)) s = 0;                  // zero block (reading Z5)
     sbyte[b] = s;
     const float db = __fmul_rn(e4m3_to_f32(s), g);  // decode scale of Eq. 2
-    const float r = rcp_approx(db);
-    const uint64_t r2 = f32x2_pack(r, r), nd2 = f32x2_pack(-db, -db);
+    const float ny = -__frcp_rn(db);
+    const uint64_t ny2 = f32x2_pack(ny, ny), db2 = f32x2_pack(db, db);
     float q[16];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint64_t x2 = f32x2_pack(v[b][2 * k], v[b][2 * k + 1]);
-      const uint64_t q0 = fmul2(x2, r2);
-      const uint64_t e = ffma2(q0, nd2, x2);  // x - q0 * d_b
-      const uint64_t q1 = ffma2(e, r2, q0);
+      const uint64_t q0 = fmul2(x2, ny2);
+      const uint64_t e = ffma2(q0, db2, x2);  // x + q0' d_b = x - q0 d_b, exact
+      const uint64_t q1 = ffma2(e, ny2, q0);
       f32x2_unpack(q1, q[2 * k], q[2 * k + 1]);
-      mn = min(mn, (__float_as_uint(q[2 * k]) + 2u) & 0x1FFFF8u);  // 0 <=> q near an E2M1 midpoint
-      mn = min(mn, (__float_as_uint(q[2 * k + 1]) + 2u) & 0x1FFFF8u);
     }
-    w0[b] = e2m1x8(q);
-    w1[b] = e2m1x8(q + 8);
+    w0[b] = e2m1x8(q) ^ 0x88888888u;
+    w1[b] = e2m1x8(q + 8) ^ 0x88888888u;
     if (s == 0) w0[b] = w1[b] = 0u;
-    if (mn == 0 && s != 0) flags |= 1u << b;
+    if (s != 0 && !(db >= 0x1p-64f)) flags |= 1u << b;
   }
   return flags;
 }
@@ -251,7 +238,8 @@ KVQ_DEV void quantize_block16(const float (&v)[16], float g, uint32_t& sbyte, ui
 #pragma unroll
   for (int k = 0; k < 16; ++k) vv[0][k] = v[k];
   uint32_t s[1], a[1], b[1];
-  if (quantize_blocks_fast<1>(vv, g, rcp_approx(g), s, a, b)) {
+  const bool g_ok = g >= 0x1p-60f && g <= 0x1p60f;  // Markstein range (see quantize_blocks_fast)
+  if (quantize_blocks_fast<1>(vv, g, __frcp_rn(g), s, a, b) || !g_ok) {
     quantize_block16_exact(v, g, sbyte, w0, w1);
     return;
   }
@@ -324,6 +312,10 @@ __global__ void __launch_bounds__(256) quant_kernel(const __grid_constant__ Quan
 #endif
 constexpr int kFusedThreads = KVQ_QUANT_THREADS;
 constexpr int kQNB = KVQ_QUANT_NB;  // blocks per thread per iteration
+#ifndef KVQ_QUANT_V_DELAY
+#define KVQ_QUANT_V_DELAY 0
+#endif
+constexpr bool kVDelay = KVQ_QUANT_V_DELAY != 0;
 
 template <int DT>
 KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
@@ -369,8 +361,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);  // bytes per 16-element block
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar[2];
-  __shared__ uint32_t red[kFusedThreads / 32];
-  __shared__ uint32_t s_amax;
+  __shared__ uint32_t red2[2][kFusedThreads / 32];
+  __shared__ uint32_t s_am[2];
   __shared__ int s_nq;
   const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
   const int64_t NU = (int64_t)p.rows * kNB;
@@ -380,6 +372,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const uint32_t slice = (uint32_t)upc * kUB;  // the V slice follows the K slice in smem
   // flagged block indices [upc]
   uint32_t* queue = reinterpret_cast<uint32_t*>(STAGED ? sm + 2 * (size_t)slice : sm);
+  if (tid < 2) s_am[tid] = 0;
   if (tid == 0) {
     s_nq = 0;
     mbar_init(bar + 0, 1);
@@ -387,28 +380,50 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  // K is requested first; V (KVQ_QUANT_V_DELAY) only once this CTA's K slice has landed, so the
+  // grid's K reads finish early and K's amax + quantization overlap V's landing.
+  auto issue = [&](int t) {
+    mbar_arrive_expect_tx(bar + t, (uint32_t)nu * kUB);
+    bulk_g2s(sm + t * slice, (const uint8_t*)p.x[t] + u0 * kUB, (uint32_t)nu * kUB, bar + t);
+  };
   if (STAGED && tid == 0 && nu > 0) {
-    for (int t = 0; t < 2; ++t) {
-      mbar_arrive_expect_tx(bar + t, (uint32_t)nu * kUB);
-      bulk_g2s(sm + t * slice, (const uint8_t*)p.x[t] + u0 * kUB, (uint32_t)nu * kUB, bar + t);
-    }
+    issue(0);
+    if (!kVDelay) issue(1);
   }
   QTRACE(0);
-  // ---- global amax of K and of V: one grid barrier for both tensors.  Each CTA max-reduces its
-  // two slices from smem, then (thread 0) a fire-and-forget red.max into this launch's amax words
-  // (double-buffered by launch parity; the other pair is cleared for the next launch) and one
-  // release-add on a monotonic arrival counter; epoch = earlier single-pass launches on this cache
-  // (host-tracked), so the barrier target is known without reading the counter first.
-  __shared__ uint32_t s_am[2];
-  if (STAGED && nu > 0) {
-    mbar_wait(bar + 0, 0);
-    mbar_wait(bar + 1, 0);
-  }
-  QTRACE(1);
-  if (p.ext_amax) {
+  // ---- global amax of K, then of V.  Barrier without fences or read-modify-write atomics: once
+  // its slice of tensor t has landed, CTA c publishes (epoch tag << 32 | its slice max) as one
+  // 64-bit store into its own 128-byte line (tag and value become visible together; one line per
+  // publisher keeps the pollers off a single L2 hot spot); then G threads of every CTA each poll one
+  // publisher's slot until its tag is this launch's epoch (epoch = earlier single-pass launches on
+  // this cache, host-tracked), and the CTA max-reduces.  Both tensors are published before K's
+  // slots are polled (quantizing K while V lands was measured slower: the code stores and the
+  // polling then compete with V's HBM reads); V's slots are loaded ahead, during K's quantization.
+  const uint32_t tag = (uint32_t)(epoch + 1);
+  if (STAGED && p.ext_amax == nullptr) {  // both slice maxima -> this CTA's slots
+    for (int t = 0; t < 2; ++t) {
+      if (nu > 0) mbar_wait(bar + t, 0);
+      if (t == 0 && kVDelay && tid == 0 && nu > 0) issue(1);
+      QTRACE(t == 0 ? 1 : 5);
+      const uint32_t lm = warp_max_u32(smem_absmax<DT>(sm + t * slice, nu * kUB));
+      if ((tid & 31) == 0) red2[t][tid >> 5] = lm;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t mm = 0;
+        for (int w = 0; w < kFusedThreads / 32; ++w) mm = max(mm, red2[t][w]);
+        const unsigned long long val = ((unsigned long long)tag << 32) | mm;
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slots + (size_t)c * kSlotU64 + t), "l"(val) : "memory");
+      }
+    }
+  } else if (p.ext_amax) {
+    if (STAGED && nu > 0) {
+      mbar_wait(bar + 0, 0);
+      if (kVDelay && tid == 0) issue(1);
+      mbar_wait(bar + 1, 0);
+    }
     if (tid < 2) s_am[tid] = __float_as_uint(p.ext_amax[tid]) & 0x7FFFFFFFu;
     __syncthreads();
-  } else if (!STAGED) {  // reduce the amax kernel's per-CTA partials
+  } else {  // two-pass: reduce the amax kernel's per-CTA partials
     uint32_t mk = 0, mv = 0;
     for (int k = tid; k < kNumPartials; k += kFusedThreads) {
       mk = max(mk, p.partials[k]);
@@ -417,79 +432,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     mk = warp_max_u32(mk);
     mv = warp_max_u32(mv);
     if ((tid & 31) == 0) {
-      red[tid >> 5] = mk;
-      queue[tid >> 5] = mv;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      mk = 0;
-      mv = 0;
-      for (int w = 0; w < kFusedThreads / 32; ++w) {
-        mk = max(mk, red[w]);
-        mv = max(mv, queue[w]);
-      }
-      s_am[0] = mk;
-      s_am[1] = mv;
-    }
-    __syncthreads();
-  } else {
-    uint32_t mk = warp_max_u32(smem_absmax<DT>(sm, nu * kUB));
-    uint32_t mv = warp_max_u32(smem_absmax<DT>(sm + slice, nu * kUB));
-    if ((tid & 31) == 0) red[tid >> 5] = mk;
-    if ((tid & 31) == 0) queue[tid >> 5] = mv;  // queue is free until the quantize loop
-    __syncthreads();
-    // Barrier without fences or atomics: CTA c publishes (epoch tag << 32 | max) for K and for V as
-    // single 64-bit stores (tag and value become visible together); then G threads of every CTA
-    // each poll one publisher's slot until its tag is this launch's epoch, and the CTA max-reduces.
-    const uint32_t tag = (uint32_t)(epoch + 1);
-    QTRACE(5);
-    if (tid == 0) {
-      mk = 0;
-      mv = 0;
-      for (int w = 0; w < kFusedThreads / 32; ++w) {
-        mk = max(mk, red[w]);
-        mv = max(mv, queue[w]);
-      }
-      const unsigned long long vk = ((unsigned long long)tag << 32) | mk, vv = ((unsigned long long)tag << 32) | mv;
-      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slots + 2 * c), "l"(vk), "l"(vv) : "memory");
-    }
-    mk = 0;
-    mv = 0;
-    if (tid < 32) {  // one warp polls (limits the polling traffic to 32 loads in flight per CTA)
-      for (int k = tid; k < G; k += 32) {
-        unsigned long long a, b;
-        for (;;) {
-          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(slots + 2 * k) : "memory");
-          if ((uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag) break;
-          __nanosleep(64);
-        }
-        mk = max(mk, (uint32_t)a);
-        mv = max(mv, (uint32_t)b);
-      }
-    }
-    QTRACE(6);
-    mk = warp_max_u32(mk);
-    mv = warp_max_u32(mv);
-    __syncthreads();
-    if ((tid & 31) == 0) {
-      red[tid >> 5] = mk;
-      queue[tid >> 5] = mv;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      mk = 0;
-      mv = 0;
-      for (int w = 0; w < kFusedThreads / 32; ++w) {
-        mk = max(mk, red[w]);
-        mv = max(mv, queue[w]);
-      }
-      s_am[0] = mk;
-      s_am[1] = mv;
+      atomicMax(&s_am[0], mk);
+      atomicMax(&s_am[1], mv);
     }
     __syncthreads();
   }
-  QTRACE(2);
+  unsigned long long pre = 0;  // V slot loaded ahead (tid < G), checked after K is quantized
   for (int t = 0; t < 2; ++t) {
+    if (STAGED && p.ext_amax == nullptr) {  // wait for every CTA's slot of tensor t
+      uint32_t m = 0;
+      for (int k = tid; k < G; k += kFusedThreads) {
+        unsigned long long a = k == tid ? pre : 0ull;
+        while ((uint32_t)(a >> 32) != tag) {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(slots + (size_t)k * kSlotU64 + t) : "memory");
+          if ((uint32_t)(a >> 32) != tag) __nanosleep(32);
+        }
+        m = max(m, (uint32_t)a);
+      }
+      if (t == 0 && tid < G)
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(pre) : "l"(slots + (size_t)tid * kSlotU64 + 1) : "memory");
+      if ((tid & ~31) < G) {  // warps that polled (whole warps: the shuffle needs all lanes)
+        m = warp_max_u32(m);
+        if ((tid & 31) == 0) atomicMax(&s_am[t], m);
+      }
+      __syncthreads();
+      QTRACE(t == 0 ? 6 : 2);
+    }
     const uint8_t* s = STAGED ? sm + t * slice : (const uint8_t*)p.x[t] + u0 * kUB;
     const uint32_t abits = s_am[t];
     if (abits >= 0x7F800000u) {  // non-finite tensor: leave the chunk undefined, report
@@ -503,7 +471,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     const float amax = __uint_as_float(abits);
     const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
-    const float rg = rcp_approx(g);
+    const float rg = __frcp_rn(g);
+    const uint32_t all_exact = g >= 0x1p-60f && g <= 0x1p60f ? 0u : (1u << kQNB) - 1;  // Markstein range
     const float invH = 1.0f / (float)p.H;
     if (c == 0 && tid == 0) p.g_out[t] = g;
     uint8_t* codes = p.codes[t];
@@ -534,7 +503,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
       }
       uint32_t sb[kQNB], w0[kQNB], w1[kQNB];
-      const uint32_t flags = quantize_blocks_fast<kQNB>(v, g, rg, sb, w0, w1);
+      const uint32_t flags = quantize_blocks_fast<kQNB>(v, g, rg, sb, w0, w1) | all_exact;
 #pragma unroll
       for (int b = 0; b < kQNB; ++b) {
         if (b > 0 && ib[b] == ib[0]) break;
@@ -742,7 +711,7 @@ cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, u
   upc = (upc + 7) & ~7;  // 128-byte aligned V slice
   const int G = (int)((NU + upc - 1) / upc);
   const size_t smem = (size_t)2 * upc * kUB + (size_t)upc * sizeof(uint32_t);  // K, V slices + flag queue
-  if (smem > 220 * 1024 || G > kNumPartials) return cudaErrorNotSupported;
+  if (smem > 220 * 1024 || G > kNumPartials || G > kMaxFusedCtas) return cudaErrorNotSupported;
   auto kern = quant_fused_kernel<DT, D, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

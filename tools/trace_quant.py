@@ -1,6 +1,6 @@
 """Phase timeline (ns, globaltimer) of the single-pass quantize kernel over all CTAs (development aid).
-Events per CTA: 0 start, 1 K landed, 2 K amax known (after the grid barrier), 3 K quantized,
-5 V landed, 6 V amax known, 7 V quantized."""
+Events per CTA: 0 start, 1 K landed, 5 V landed, 6 K amax known (after polling every CTA's slot),
+4 K fast path done, 3 K quantized, 2 V amax known, 7 V quantized."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -24,6 +24,6 @@ t = tr.view(256, 8).cpu().numpy().astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 t = t - t0
-names = {0: "start", 1: "landed", 5: "local amax", 6: "polled", 2: "amax", 4: "K fast", 3: "K quant", 7: "V quant"}
+names = {0: "start", 1: "K landed", 5: "V landed", 6: "K amax", 4: "K fast", 3: "K quant", 2: "V amax", 7: "V quant"}
 print(f"{len(t)} CTAs: " + "  ".join(f"{n}: min {t[:, e].min()} med {int(np.median(t[:, e]))} max {t[:, e].max()}"
                                      for e, n in names.items()))
