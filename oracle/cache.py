@@ -19,7 +19,13 @@ from .keyset import key_token_ranges
 
 
 class OracleKVCache:
-    def __init__(self, num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk):
+    """``scale_search`` = Four-Over-Six block scales for K and V (PAPER.md:146, 728-739);
+    ``k_smoothing`` = keys mean-centred per (t, h) row, mean restored on dequantization
+    (readings Z20-Z22)."""
+
+    def __init__(self, num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk,
+                 scale_search=False, k_smoothing=False):
+        self.scale_search, self.k_smoothing = bool(scale_search), bool(k_smoothing)
         self.L, self.H, self.d = num_layers, num_heads, head_dim
         self.tpf, self.fc = tokens_per_frame, frames_per_chunk
         self.Tc = tokens_per_frame * frames_per_chunk
@@ -27,7 +33,9 @@ class OracleKVCache:
 
     def append(self, layer, chunk_index, K, V):
         """kv_quantize_append: quantize K and V of one chunk."""
-        self.chunks[layer][int(chunk_index)] = (nvfp4.quantize_kv_chunk(K), nvfp4.quantize_kv_chunk(V))
+        self.chunks[layer][int(chunk_index)] = (
+            nvfp4.quantize_kv_chunk(K, self.scale_search, smooth=self.k_smoothing),
+            nvfp4.quantize_kv_chunk(V, self.scale_search))
 
     def export(self, layer, chunk_index):
         qk, qv = self.chunks[layer][int(chunk_index)]
