@@ -60,8 +60,17 @@ typedef struct {
   int32_t sink_frames;      /* S_g of the global sink A_g, pinned, never evicted */
   int32_t window_frames;    /* sliding window W in frames INCLUDING the current chunk (reading Z10) */
   int32_t max_chunk_slots;  /* slots per layer; >= sink chunks + window chunks (+ shot chunks) */
-  int32_t scale_mode;       /* 0 = block scale amax/6.  Other values: KVQ_EINVAL */
-  int32_t k_smoothing;      /* 0.  K-smoothing is a later row: KVQ_EINVAL */
+  int32_t scale_mode;       /* 0 = block scale alpha_i(6) = cast_E4M3(max|U_bar|/6);
+                               1 = Four-Over-Six search between alpha_i(6) and alpha_i(4) for K and V
+                               (Eq. 4o6, applied to KV by PAPER.md:146): the
+                               candidate with the lower float32 squared reconstruction error wins,
+                               ties to 6 (reading Z21).  Other values: KVQ_EINVAL */
+  int32_t k_smoothing;      /* 0 = off; 1 = K-smoothing: keys are stored as
+                               K_bar = K - mean_d(K) per (t, h) row (float32 tree-order mean,
+                               reading Z20); the fp32 row means are stored with the chunk and
+                               restored exactly (K^ = dequant(K_bar) + mean) by kv_dequantize and
+                               by chunk_attention (as the rank-1 score term mean_j * sum_u Q_iu).
+                               Other values: KVQ_EINVAL */
 } kvq_config;
 
 /* Key set of one attention call: K_eff(t) = A_g U A_s U KV_[t-W,t) U {chunk t}, deduplicated
@@ -126,7 +135,8 @@ kvq_status chunk_attention(kvq_cache* cache, int32_t layer, const void* Q, kvq_d
                            kvq_dtype out_dtype, void* stream);
 
 /* Checking: dequantize one resident chunk to dev [T_c, H, d]: FP32 = RN32(dec(c) dec(s) g)
- * (Eq. 2), BF16 = RN_bf16 of that. */
+ * (Eq. 2), BF16 = RN_bf16 of that.  With k_smoothing, K = RN32(dec(c) dec(s) g + mean)
+ * (one rounding). */
 kvq_status kv_dequantize(const kvq_cache* cache, int32_t layer, int64_t chunk_index,
                          void* K_out, void* V_out, kvq_dtype out_dtype, void* stream);
 
@@ -135,6 +145,11 @@ kvq_status kv_dequantize(const kvq_cache* cache, int32_t layer, int64_t chunk_in
 kvq_status kv_export_chunk(const kvq_cache* cache, int32_t layer, int64_t chunk_index,
                            void* codes_k, void* scales_k, float* g_k,
                            void* codes_v, void* scales_v, float* g_v, void* stream);
+
+/* K-smoothing row means of one resident chunk: dev fp32 [T_c*H], rows (t, h) t-major.
+ * KVQ_EINVAL when the cache was created with k_smoothing = 0; KVQ_ENOCHUNK if not resident. */
+kvq_status kv_export_kmean(const kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                           float* mean_out, void* stream);
 
 /* Bytes of resident NVFP4 K/V payload (codes + scales + tensor scales) over all layers'
  * resident chunks -- the footprint report for PAPER.md:146's "close to 3.6x". */

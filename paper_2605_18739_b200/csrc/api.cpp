@@ -27,6 +27,7 @@ struct Layout {
   int64_t T_c, T_pad, rows_per_head;  // rows_per_head = slots * T_pad
   size_t codes_bytes, scales_bytes;   // per tensor (K or V), all layers
   size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_counters, off_ws, total;
+  size_t off_mean, mean_bytes;        // K-smoothing row means [L][H][rows_per_head] fp32 (0 if off)
 };
 
 bool valid_cfg(const kvq_config* c) {
@@ -36,7 +37,7 @@ bool valid_cfg(const kvq_config* c) {
   if (c->tokens_per_frame <= 0 || c->frames_per_chunk <= 0) return false;
   if (c->sink_frames < 0 || c->window_frames < c->frames_per_chunk) return false;
   if (c->max_chunk_slots <= 0) return false;
-  if (c->scale_mode != 0 || c->k_smoothing != 0) return false;
+  if ((c->scale_mode != 0 && c->scale_mode != 1) || (c->k_smoothing != 0 && c->k_smoothing != 1)) return false;
   int64_t Tc = (int64_t)c->tokens_per_frame * c->frames_per_chunk;
   if (Tc > (1 << 24)) return false;
   return true;
@@ -61,6 +62,8 @@ Layout make_layout(const kvq_config* c) {
   L.off_counters = off;  // grid-barrier slots of the single-pass quantizer: [CTA][K|V] u64
   off += align_up((size_t)kMaxFusedCtas * kSlotU64 * sizeof(unsigned long long), kAlign);
   L.off_ws = off; off += align_up(attn_ws_bytes(c->head_dim), kAlign);
+  L.mean_bytes = c->k_smoothing ? align_up((size_t)rows * sizeof(float), kAlign) : 0;
+  L.off_mean = off; off += L.mean_bytes;
   L.total = off;
   return L;
 }
@@ -110,6 +113,14 @@ uint8_t* scales_base(const kvq_cache* c, int t, int layer) {
 }
 float* g_base(const kvq_cache* c, int layer) {
   return reinterpret_cast<float*>(c->arena + c->L.off_g) + (size_t)layer * c->cfg.max_chunk_slots * 2;
+}
+// K-smoothing row means of (layer, head 0, slot 0), head-major like the scales; null when off
+float* mean_base(const kvq_cache* c, int layer) {
+  if (!c->cfg.k_smoothing) return nullptr;
+  return reinterpret_cast<float*>(c->arena + c->L.off_mean) + (size_t)layer * c->cfg.num_heads * c->L.rows_per_head;
+}
+int quant_mode(const kvq_cache* c) {
+  return (c->cfg.scale_mode == 1 ? kModeSearch : 0) | (c->cfg.k_smoothing ? kModeSmoothK : 0);
 }
 DevStatus* status_ptr(const kvq_cache* c) { return reinterpret_cast<DevStatus*>(c->arena + c->L.off_status); }
 
@@ -228,6 +239,9 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   p.status = status_ptr(c);
   p.trace = kvq_trace_ptr();
   p.epoch = c->quant_epoch;
+  p.mode = quant_mode(c);
+  p.mean_out = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
+  p.partials_w = partials;
   // single pass when the chunk fits in aggregate shared memory, else amax pass + quantize pass
   cudaError_t e = c->two_pass_only ? cudaErrorNotSupported
                                    : launch_quantize_fused(p, reinterpret_cast<unsigned long long*>(c->arena + c->L.off_counters),
@@ -235,7 +249,12 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   if (e == cudaSuccess && !ext_amax) c->quant_epoch++;  // the launch arrives G times on each counter
   if (e == cudaErrorNotSupported) {
     (void)cudaGetLastError();
-    if (!ext_amax) {
+    if (c->cfg.k_smoothing) {  // K row means (+ K_bar partials), then V's partials
+      e = launch_smooth_amax(p, st);
+      if (e == cudaSuccess && !ext_amax)
+        e = launch_amax(K, V, dt == KVQ_BF16 ? DT_BF16 : DT_FP32, rows * d, partials, status_ptr(c), st, 1);
+      if (e != cudaSuccess) return KVQ_ECUDA;
+    } else if (!ext_amax) {
       e = launch_amax(K, V, dt == KVQ_BF16 ? DT_BF16 : DT_FP32, rows * d, partials, status_ptr(c), st);
       if (e != cudaSuccess) return KVQ_ECUDA;
     }
@@ -333,6 +352,7 @@ kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype
   p.q_dtype = q_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
   p.O = O;
   p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.mean_k = mean_base(c, layer);
   p.codes_k = codes_base(c, 0, layer);
   p.codes_v = codes_base(c, 1, layer);
   p.scales_k = scales_base(c, 0, layer);
@@ -369,6 +389,7 @@ kvq_status kv_dequantize(const kvq_cache* c, int32_t layer, int64_t chunk, void*
   p.T = (int)c->L.T_c;
   p.H = c->cfg.num_heads;
   p.d = d;
+  p.mean = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
   p.out[0] = K_out;
   p.out[1] = V_out;
   p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
@@ -401,11 +422,28 @@ kvq_status kv_export_chunk(const kvq_cache* c, int32_t layer, int64_t chunk, voi
   return cuda_status(launch_export(p, S(stream)));
 }
 
+kvq_status kv_export_kmean(const kvq_cache* c, int32_t layer, int64_t chunk, float* mean_out, void* stream) {
+  if (!c || !mean_out || layer < 0 || layer >= c->cfg.num_layers) return KVQ_EINVAL;
+  if (!c->cfg.k_smoothing) return KVQ_EINVAL;
+  auto it = c->layers[layer].slot_of.find(chunk);
+  if (it == c->layers[layer].slot_of.end()) return KVQ_ENOCHUNK;
+  const int slot = it->second;
+  ExportParams p{};
+  p.head_stride_rows = c->L.rows_per_head;
+  p.T = (int)c->L.T_c;
+  p.H = c->cfg.num_heads;
+  p.d = c->cfg.head_dim;
+  p.mean = mean_base(c, layer) + (size_t)slot * c->L.T_pad;
+  p.mean_out = mean_out;
+  return cuda_status(launch_export(p, S(stream)));
+}
+
 size_t kvq_resident_bytes(const kvq_cache* c) {
   if (!c) return 0;
   size_t n = 0;
   const size_t rows = (size_t)c->L.T_c * c->cfg.num_heads;
-  const size_t per_chunk = 2 * (rows * (c->cfg.head_dim / 2) + rows * (c->cfg.head_dim / 16) + sizeof(float));
+  const size_t per_chunk = 2 * (rows * (c->cfg.head_dim / 2) + rows * (c->cfg.head_dim / 16) + sizeof(float)) +
+                           (c->cfg.k_smoothing ? rows * sizeof(float) : 0);  // + K row means
   for (auto& ls : c->layers) n += ls.slot_of.size() * per_chunk;
   return n;
 }
@@ -433,6 +471,7 @@ kvq_status kv_dequantize_window(const kvq_cache* c, int32_t layer, const kvq_mas
   p.scales[0] = scales_base(c, 0, layer);
   p.scales[1] = scales_base(c, 1, layer);
   p.g = g_base(c, layer);
+  p.mean = mean_base(c, layer);
   p.head_stride_rows = c->L.rows_per_head;
   p.T = (int)c->L.T_pad;
   p.H = c->cfg.num_heads;

@@ -65,7 +65,8 @@ struct WsSmem {
   static constexpr int kV1 = 5 * kTile;
   static constexpr int kBar = 6 * kTile;
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
-  static constexpr int kBytes = kBar + 16 * 8 + 16 + 1024;
+  static constexpr int kMean = kBar + 16 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
+  static constexpr int kBytes = kMean + 2 * 2 * 128 * 4 + 1024;
 };
 
 // address of 16-byte chunk c (8 consecutive elements along d) of row r in a 128-row tile
@@ -131,9 +132,11 @@ KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool val
   }
 }
 
-// Q row -> fp16 (bf16 in bf16-KV mode) into a tile row
-template <int D, bool MMA_BF16>
-KVQ_DEV void load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_t row_index, bool valid) {
+// Q row -> fp16 (bf16 in bf16-KV mode) into a tile row.  SUM: also returns sum_u Q_iu of the
+// rounded values (fp32; the K-smoothing restitution term, see attn_ws_kernel).
+template <int D, bool MMA_BF16, bool SUM = false>
+KVQ_DEV float load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_t row_index, bool valid) {
+  float qsum = 0.0f;
 #pragma unroll
   for (int c = 0; c < D / 8; ++c) {
     uint32_t o[4] = {0, 0, 0, 0};
@@ -157,8 +160,16 @@ KVQ_DEV void load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_
           o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
       }
     }
+    if (SUM) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&o[k]));
+        qsum += f2.x + f2.y;
+      }
+    }
     st_shared_v4(chunk_addr(base, r, c), o[0], o[1], o[2], o[3]);
   }
+  return qsum;
 }
 
 // Tile iteration over the key segments: tile = 128 slot-aligned rows, valid rows [lo, hi).
@@ -238,7 +249,11 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
       p.trace[(tile) * 16 + (ev)] = clock64();                                                   \
   } while (0)
 
-template <int D, bool NVFP4, bool MMA_BF16>
+// SMOOTH (K-smoothing, reading Z20): the cache holds K_bar = K - m per key row,
+// and the score is restored exactly as q.k = q.k_bar + m_j sum_u q_u -- a rank-1 term added in
+// fp32 to the scaled MMA scores before the row max, from the fp32 row sum of the (rounded) Q row
+// and the key means of the tile (one coalesced load per softmax thread, shared through smem).
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH>
 __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
   using SM = WsSmem<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -298,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
-      load_q_row<D, MMA_BF16>(SQ(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      const float qsum = load_q_row<D, MMA_BF16, SMOOTH>(SQ(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      const uint64_t qsb2 = f32x2_pack(qsum * p.scale_log2, qsum * p.scale_log2);
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
       float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
@@ -313,6 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           gv = __ldg(p.g + 2 * sg.slot + 1);
         }
         const float cs = gk * p.scale_log2;
+        float mean_r = 0.0f;  // SMOOTH: this thread's key of the tile
+        if (SMOOTH && row >= lo && row < hi)
+          mean_r = __ldg(p.mean_k + (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + row);
         KVQ_TRACE(g, 3 * qi + 0);
         mbar_wait(sfull + qi, g & 1);
         KVQ_TRACE(g, 3 * qi + 1);
@@ -320,8 +339,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         uint32_t s[128];
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) KVQ_TMEM_LD32(tS + 32 * cc, (s + 32 * cc));
+        if (SMOOTH) {  // share the tile's key means within the warpgroup (double-buffered)
+          float* mbuf = reinterpret_cast<float*>(smem + SM::kMean) + (qi * 2 + (j & 1)) * 128;
+          mbuf[row] = mean_r;
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + qi) : "memory");
+        }
         tmem_ld_wait();
-        // row max of raw scores over valid keys (scale cs > 0 commutes with max)
+        if (SMOOTH) {  // y = s * cs + m_j * sum(q) * scale_log2  (log2 units), in place
+          const float* mbuf = reinterpret_cast<const float*>(smem + SM::kMean) + (qi * 2 + (j & 1)) * 128;
+          const uint64_t cs2s = f32x2_pack(cs, cs);
+#pragma unroll
+          for (int kk = 0; kk < 64; ++kk) {
+            const float2 m2 = reinterpret_cast<const float2*>(mbuf)[kk];
+            const uint64_t b2 = fmul2(f32x2_pack(m2.x, m2.y), qsb2);
+            const uint64_t y2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2s, b2);
+            float y0, y1;
+            f32x2_unpack(y2, y0, y1);
+            s[2 * kk] = __float_as_uint(y0);
+            s[2 * kk + 1] = __float_as_uint(y1);
+          }
+        }
+        // row max over valid keys (raw scores: the scale cs > 0 commutes with max)
         if (lo != 0 || hi != 128) {
 #pragma unroll
           for (int kk = 0; kk < 128; ++kk)
@@ -344,12 +382,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         // than kLazyLog2 (P <= 2^kLazyLog2, far inside fp16); otherwise O needs no rescale.  The row
         // sum l is taken from the fp16-ROUNDED P (the weights the PV MMA actually uses), so the
         // normalisation stays exactly consistent for peaked rows.
-        const float m_tile = mx * cs;
+        const float m_tile = SMOOTH ? mx : mx * cs;
         const float m_new = (j == 0 || m_tile > m_run + kLazyLog2) ? fmaxf(m_run, m_tile) : m_run;
 #endif
         const float alpha = ex2_approx(m_run - m_new);
         // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp16-rounded p (two packed chains)
-        const uint64_t cs2 = f32x2_pack(cs, cs), mneg2 = f32x2_pack(-m_new, -m_new);
+        const float cse = SMOOTH ? 1.0f : cs;  // SMOOTH: s already holds the scaled, restored score
+        const uint64_t cs2 = f32x2_pack(cse, cse), mneg2 = f32x2_pack(-m_new, -m_new);
         uint64_t acc0 = 0, acc1 = 0;
         float la[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -651,9 +690,9 @@ __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ At
   }
 }
 
-template <int D, bool NVFP4, bool MMA_BF16>
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH = false>
 cudaError_t launch_t(AttnParams p, cudaStream_t st) {
-  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16>;
+  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16, SMOOTH>;
   const int smem = WsSmem<D>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -684,6 +723,8 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st) {
+  if (nvfp4_kv && p.mean_k)
+    return p.d == 128 ? launch_t<128, true, false, true>(p, st) : launch_t<64, true, false, true>(p, st);
   if (nvfp4_kv) return p.d == 128 ? launch_t<128, true, false>(p, st) : launch_t<64, true, false>(p, st);
   return p.d == 128 ? launch_t<128, false, true>(p, st) : launch_t<64, false, true>(p, st);
 }

@@ -12,6 +12,9 @@ constexpr int kSlotU64 = 16;        // one 128-byte line per barrier slot: [K, V
 constexpr int kMaxSegs = 48;       // key segments per attention call
 
 enum DType : int { DT_BF16 = 0, DT_FP32 = 1, DT_FP16 = 2 };
+// quantizer modes (§8(f)): Four-Over-Six block-scale search for K and V; K-smoothing of K
+constexpr int kModeSearch = 1;
+constexpr int kModeSmoothK = 2;
 
 // Device status word (in the arena): code (0 = ok), then first bad flat index.
 struct DevStatus {
@@ -33,12 +36,16 @@ struct QuantParams {
   unsigned long long* trace; // debug timeline (null in production)
   unsigned long long epoch;  // single-pass launches so far on this cache (grid-barrier target)
   DevStatus* status;
+  int mode;                  // kModeSearch | kModeSmoothK bits
+  float* mean_out;           // K-smoothing: K row means, slot base for head 0, [H][head_stride_rows]
+  uint32_t* partials_w;      // two-pass smoothing: where smooth_amax_kernel writes K's partials
 };
 
 struct DequantParams {
   const uint8_t* codes[2];
   const uint8_t* scales[2];
   const float* g;            // [2]
+  const float* mean;         // K-smoothing row means (slot base, head-major like scales) or null
   int64_t head_stride_rows;
   int T, H, d;
   void* out[2];              // [T, H, d]
@@ -54,6 +61,8 @@ struct ExportParams {
   uint8_t* codes_out[2];
   uint8_t* scales_out[2];
   float* g_out[2];
+  const float* mean;         // K-smoothing row means (slot base) or null
+  float* mean_out;           // [T*H] t-major, or null
 };
 
 struct AttnSeg {
@@ -73,6 +82,7 @@ struct AttnParams {
   const uint8_t* scales_k;
   const uint8_t* scales_v;
   const float* g;            // g[slot*2 + {0,1}]
+  const float* mean_k;       // K-smoothing row means (layer base, head-major like the codes) or null
   int64_t head_stride_rows;  // slots * T_pad
   int T_pad;                 // rows per slot (multiple of 128)
   // bf16 KV mode: K, V [n_keys, H, d]
@@ -94,10 +104,11 @@ struct AttnParams {
 constexpr int kMaxCtas = 148;  // workspace sized for one CTA per SM on B200
 inline size_t attn_ws_bytes(int d) { return (size_t)2 * kMaxCtas * (256 * d + 512) * sizeof(float); }
 
+// tsr_begin = 1: V only (K's partials then come from launch_smooth_amax)
+cudaError_t launch_smooth_amax(const QuantParams& p, cudaStream_t st);
 cudaError_t launch_amax(const void* K, const void* V, int dtype, int64_t n, uint32_t* partials,
-                        DevStatus* status, cudaStream_t st);
-cudaError_t launch_quantize(const QuantParams& p, cudaStream_t st);
-// second pass of the two-launch path (after launch_amax), deferred-exact per-block work
+                        DevStatus* status, cudaStream_t st, int tsr_begin = 0);
+// second pass of the two-launch path (after the amax pass)
 cudaError_t launch_quantize2(const QuantParams& p, int sms, cudaStream_t st);
 // single-pass cooperative quantize/append; cudaErrorNotSupported when the chunk does not fit
 cudaError_t launch_quantize_fused(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,

@@ -56,9 +56,9 @@ KVQ_DEV uint32_t vec_absmax_bits(uint4 v) {
 
 template <int DT>
 __global__ void __launch_bounds__(256) amax_kernel(const void* K, const void* V, int64_t n, uint32_t* partials,
-                                                   DevStatus* status) {
+                                                   DevStatus* status, int tsr_base) {
   constexpr int kPer = DT == DT_BF16 ? 8 : 4;  // elements per 16-byte vector
-  const int tsr = blockIdx.y;
+  const int tsr = blockIdx.y + tsr_base;
   const uint8_t* x = (const uint8_t*)(tsr ? V : K);
   const int64_t nvec = n / kPer;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -174,7 +174,57 @@ KVQ_DEV float div_markstein(float a, float b, float rb) {
 // E2M1 codes of the negation are flipped back with one XOR per 8 codes.  The theorem's range
 // conditions hold for 2^-60 <= g <= 2^60 (checked per tensor by the caller) and d_b >= 2^-64
 // (checked here: bit b of the return value sends block b through quantize_block16_exact).
-template <int NB>
+KVQ_DEV uint32_t scale_byte(float u, float bmax) {
+  uint32_t s = e4m3_from_f32(u);
+  if (s == 0) s = 1;              // SPEC.md:191 underflow promotion
+  if (!(bmax > 0.0f)) s = 0;      // zero block (reading Z5)
+  return s;
+}
+
+KVQ_DEV void codes_markstein(const float (&v)[16], float db, uint32_t& w0, uint32_t& w1) {
+  const float ny = -__frcp_rn(db);
+  const uint64_t ny2 = f32x2_pack(ny, ny), db2 = f32x2_pack(db, db);
+  float q[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t x2 = f32x2_pack(v[2 * k], v[2 * k + 1]);
+    const uint64_t q0 = fmul2(x2, ny2);
+    const uint64_t e = ffma2(q0, db2, x2);  // x + q0' d_b = x - q0 d_b, exact
+    const uint64_t q1 = ffma2(e, ny2, q0);
+    f32x2_unpack(q1, q[2 * k], q[2 * k + 1]);
+  }
+  w0 = e2m1x8(q) ^ 0x88888888u;
+  w1 = e2m1x8(q + 8) ^ 0x88888888u;
+}
+
+// Squared reconstruction error of one block under (codes w0 w1, scale byte s) in float32, the
+// quantity Four-Over-Six compares (reading Z21): r_i = RN32(x_i - dec(c_i) dec(s) g)
+// (dec(c) dec(s) is exact in f16 -- <= 6 significant bits within [2^-10, 2688] -- and the FMA
+// rounds once), A / B = FMA chains r_i^2 + acc over the even / odd elements in ascending order
+// (one FFMA2 chain on element pairs), E = RN32(A + B).
+KVQ_DEV float block_sse(const float (&v)[16], uint32_t w0, uint32_t w1, uint32_t s, float g) {
+  const uint32_t s2 = f16x2_from_e4m3x2(s | (s << 8));
+  uint32_t o[8];
+  dequant_word_f16(w0, s2, *reinterpret_cast<uint32_t(*)[4]>(o));
+  dequant_word_f16(w1, s2, *reinterpret_cast<uint32_t(*)[4]>(o + 4));
+  const uint64_t ng2 = f32x2_pack(-g, -g);
+  uint64_t acc = f32x2_pack(0.0f, 0.0f);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float lo = __half2float(__ushort_as_half((unsigned short)(o[k] & 0xFFFF)));
+    const float hi = __half2float(__ushort_as_half((unsigned short)(o[k] >> 16)));
+    const uint64_t r = ffma2(f32x2_pack(lo, hi), ng2, f32x2_pack(v[2 * k], v[2 * k + 1]));
+    acc = ffma2(r, r, acc);
+  }
+  float a, b;
+  f32x2_unpack(acc, a, b);
+  return __fadd_rn(a, b);
+}
+
+// NB blocks (independent streams for latency hiding).  SEARCH = Four-Over-Six:
+// the 4-target candidate alpha_i(4) = cast_E4M3(RN32(t/4)) (t/4 is an exact scaling) replaces the
+// 6-target one when its float32 error is strictly lower (ties to 6).
+template <int NB, bool SEARCH>
 KVQ_DEV uint32_t quantize_blocks_fast(const float (&v)[NB][16], float g, float rg, uint32_t (&sbyte)[NB],
                                       uint32_t (&w0)[NB], uint32_t (&w1)[NB]) {
   uint32_t flags = 0;
@@ -188,33 +238,41 @@ KVQ_DEV uint32_t quantize_blocks_fast(const float (&v)[NB][16], float g, float r
     }
     const float bmax = fmaxf(m0, m1);
     const float t = div_markstein(bmax, g, rg);
-    const float u = div_markstein(t, 6.0f, 0.16666667163372040f);  // RN32(1/6)
-    uint32_t s = e4m3_from_f32(u);
-    if (s == 0) s = 1;                          // SPEC.md:191 underflow promotion
-    if (!(bmax > 0.0f)) s = 0;                  // zero block (reading Z5)
-    sbyte[b] = s;
+    uint32_t s = scale_byte(div_markstein(t, 6.0f, 0.16666667163372040f), bmax);  // RN32(1/6)
     const float db = __fmul_rn(e4m3_to_f32(s), g);  // decode scale of Eq. 2
-    const float ny = -__frcp_rn(db);
-    const uint64_t ny2 = f32x2_pack(ny, ny), db2 = f32x2_pack(db, db);
-    float q[16];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint64_t x2 = f32x2_pack(v[b][2 * k], v[b][2 * k + 1]);
-      const uint64_t q0 = fmul2(x2, ny2);
-      const uint64_t e = ffma2(q0, db2, x2);  // x + q0' d_b = x - q0 d_b, exact
-      const uint64_t q1 = ffma2(e, ny2, q0);
-      f32x2_unpack(q1, q[2 * k], q[2 * k + 1]);
-    }
-    w0[b] = e2m1x8(q) ^ 0x88888888u;
-    w1[b] = e2m1x8(q + 8) ^ 0x88888888u;
-    if (s == 0) w0[b] = w1[b] = 0u;
+    codes_markstein(v[b], db, w0[b], w1[b]);
     if (s != 0 && !(db >= 0x1p-64f)) flags |= 1u << b;
+    if (SEARCH) {
+      const uint32_t s4 = scale_byte(__fmul_rn(t, 0.25f), bmax);
+      if (s4 != s) {
+        const float db4 = __fmul_rn(e4m3_to_f32(s4), g);
+        uint32_t a0, a1;
+        codes_markstein(v[b], db4, a0, a1);
+        if (!(db4 >= 0x1p-64f)) flags |= 1u << b;
+        if (block_sse(v[b], a0, a1, s4, g) < block_sse(v[b], w0[b], w1[b], s, g)) {
+          s = s4;
+          w0[b] = a0;
+          w1[b] = a1;
+        }
+      }
+    }
+    sbyte[b] = s;
+    if (s == 0) w0[b] = w1[b] = 0u;
   }
   return flags;
 }
 
-// The definition itself, with IEEE divisions (reading Z4, R1): the reference path for flagged
-// blocks and for the two-pass fallback.
+// The definition itself, with IEEE divisions (reading Z4, R1; Four-Over-Six as above): the
+// reference path for flagged blocks.
+KVQ_DEV void codes_exact(const float (&v)[16], float db, uint32_t& w0, uint32_t& w1) {
+  float q[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) q[k] = __fdiv_rn(v[k], db);
+  w0 = e2m1x8(q);
+  w1 = e2m1x8(q + 8);
+}
+
+template <bool SEARCH>
 KVQ_DEV void quantize_block16_exact(const float (&v)[16], float g, uint32_t& sbyte, uint32_t& w0, uint32_t& w1) {
   float bmax = 0.0f;
 #pragma unroll
@@ -223,77 +281,129 @@ KVQ_DEV void quantize_block16_exact(const float (&v)[16], float g, uint32_t& sby
   w0 = 0;
   w1 = 0;
   if (!(bmax > 0.0f)) return;
-  sbyte = e4m3_from_f32(__fdiv_rn(__fdiv_rn(bmax, g), 6.0f));
-  if (sbyte == 0) sbyte = 1;
-  const float db = __fmul_rn(e4m3_to_f32(sbyte), g);
-  float q[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) q[k] = __fdiv_rn(v[k], db);
-  w0 = e2m1x8(q);
-  w1 = e2m1x8(q + 8);
-}
-
-KVQ_DEV void quantize_block16(const float (&v)[16], float g, uint32_t& sbyte, uint32_t& w0, uint32_t& w1) {
-  float vv[1][16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) vv[0][k] = v[k];
-  uint32_t s[1], a[1], b[1];
-  const bool g_ok = g >= 0x1p-60f && g <= 0x1p60f;  // Markstein range (see quantize_blocks_fast)
-  if (quantize_blocks_fast<1>(vv, g, __frcp_rn(g), s, a, b) || !g_ok) {
-    quantize_block16_exact(v, g, sbyte, w0, w1);
-    return;
+  const float t = __fdiv_rn(bmax, g);
+  sbyte = scale_byte(__fdiv_rn(t, 6.0f), bmax);
+  codes_exact(v, __fmul_rn(e4m3_to_f32(sbyte), g), w0, w1);
+  if (SEARCH) {
+    const uint32_t s4 = scale_byte(__fdiv_rn(t, 4.0f), bmax);
+    if (s4 != sbyte) {
+      uint32_t a0, a1;
+      codes_exact(v, __fmul_rn(e4m3_to_f32(s4), g), a0, a1);
+      if (block_sse(v, a0, a1, s4, g) < block_sse(v, w0, w1, sbyte, g)) {
+        sbyte = s4;
+        w0 = a0;
+        w1 = a1;
+      }
+    }
   }
-  sbyte = s[0];
-  w0 = a[0];
-  w1 = b[0];
 }
 
-template <int DT, int D>
-__global__ void __launch_bounds__(256) quant_kernel(const __grid_constant__ QuantParams p) {
-  constexpr int kNB = D / 16;                 // blocks per row
-  constexpr int kES = DT == DT_BF16 ? 2 : 4;  // input element bytes
-  const int tsr = blockIdx.y;
-  __shared__ uint32_t red[8];
+// K-smoothing, reading Z20: the row mean is the float32 sum in a fixed tree
+// order times 1/d.  Within a 16-element block: y_k = x_k + x_{k+8}, z_k = y_k + y_{k+4},
+// w_k = z_k + z_{k+2}, S = w_0 + w_1 (three FADD2 levels on element pairs, one FADD); across the
+// d/16 blocks of a row (held by d/16 consecutive lanes): a butterfly, ((S0+S1)+(S2+S3))+... --
+// every lane ends with the same bits because float addition is commutative.
+KVQ_DEV float block_sum16(const float (&v)[16]) {
+  uint64_t a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = f32x2_pack(v[2 * k], v[2 * k + 1]);
+  const uint64_t c0 = fadd2(fadd2(a[0], a[4]), fadd2(a[2], a[6]));
+  const uint64_t c1 = fadd2(fadd2(a[1], a[5]), fadd2(a[3], a[7]));
+  float lo, hi;
+  f32x2_unpack(fadd2(c0, c1), lo, hi);
+  return __fadd_rn(lo, hi);
+}
 
-  // ---- tensor amax -> g = RN32(amax / (448 * 6)) (reading Z1), amax = 0 -> 1
-  uint32_t abits;
-  if (p.ext_amax) {
-    abits = __float_as_uint(p.ext_amax[tsr]) & 0x7FFFFFFFu;
+template <int KNB>
+KVQ_DEV float row_mean(const float (&v)[16]) {
+  float s = block_sum16(v);
+#pragma unroll
+  for (int o = 1; o < KNB; o <<= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return __fmul_rn(s, 1.0f / (16 * KNB));  // exact: 1/d is a power of two
+}
+
+KVQ_DEV void subtract_mean(float (&v)[16], float m) {
+  const uint64_t nm2 = f32x2_pack(-m, -m);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t x2 = fadd2(f32x2_pack(v[2 * k], v[2 * k + 1]), nm2);  // RN32(x - m)
+    f32x2_unpack(x2, v[2 * k], v[2 * k + 1]);
+  }
+}
+
+// |x - m| max of a block as float bits; a non-finite mean (some x non-finite) -> +inf bits
+KVQ_DEV uint32_t smoothed_absmax_bits(const float (&v)[16], float m) {
+  float x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = v[k];
+  subtract_mean(x, m);
+  float m0 = 0.0f, m1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 16; k += 4) {
+    m0 = fmax3(m0, fabsf(x[k]), fabsf(x[k + 1]));
+    m1 = fmax3(m1, fabsf(x[k + 2]), fabsf(x[k + 3]));
+  }
+  const uint32_t bits = __float_as_uint(fmaxf(m0, m1));
+  return fabsf(m) <= 3.402823466e38f ? bits : 0x7F800000u;
+}
+
+template <int DT>
+KVQ_DEV void unpack_block16(const uint8_t* src, float (&v)[16]) {  // generic pointer (smem or global)
+  if (DT == DT_BF16) {
+    const uint4 x0 = *reinterpret_cast<const uint4*>(src), x1 = *reinterpret_cast<const uint4*>(src + 16);
+    const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
   } else {
-    uint32_t m = 0;
-    for (int i = threadIdx.x; i < kNumPartials; i += blockDim.x) m = max(m, p.partials[tsr * kNumPartials + i]);
-    m = warp_max_u32(m);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    m = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) m = max(m, red[w]);
-    abits = m;
+    for (int k = 0; k < 4; ++k) {
+      const float4 x = reinterpret_cast<const float4*>(src)[k];
+      v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+    }
   }
-  if (abits >= 0x7F800000u) {  // non-finite tensor: leave the chunk undefined, report
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&p.status->code, 0, -6);
-    return;
-  }
-  const float amax = __uint_as_float(abits);
-  const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.g_out[tsr] = g;
+}
 
-  const uint8_t* x = (const uint8_t*)p.x[tsr];
-  uint8_t* codes = p.codes[tsr];
-  uint8_t* scales = p.scales[tsr];
-  const int64_t total = (int64_t)p.rows * kNB;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < total; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = b / kNB;
-    const int j = (int)(b - row * kNB);
+// Two-pass path, K with smoothing: per block (thread), row means by lane butterfly, written to the
+// head-major mean slot; per-CTA max |K_bar| into partials[0][blockIdx.x] (grid = kNumPartials).
+template <int DT, int D>
+__global__ void __launch_bounds__(256) smooth_amax_kernel(const __grid_constant__ QuantParams p) {
+  constexpr int kNB = D / 16;
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
+  const int64_t NU = (int64_t)p.rows * kNB;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint32_t m = 0;
+  // warp-uniform trip count: the row butterfly needs every lane
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < NU; base += stride) {
+    const int64_t u = base + (threadIdx.x & 31);
+    const bool valid = u < NU;
     float v[16];
-    load_block16<DT>(x + (row * D + j * 16) * kES, v);
-    uint32_t sbyte, w0, w1;
-    quantize_block16(v, g, sbyte, w0, w1);
-    const int t_tok = (int)(row / p.H);
-    const int h = (int)(row - (int64_t)t_tok * p.H);
-    const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
-    *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(w0, w1);
-    scales[orow * kNB + j] = (uint8_t)sbyte;
+    if (valid) {
+      load_block16<DT>((const uint8_t*)p.x[0] + u * kUB, v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
+    }
+    const float mean = row_mean<kNB>(v);
+    if (valid) {
+      m = max(m, smoothed_absmax_bits(v, mean));
+      const int64_t row = u / kNB;
+      if (u - row * kNB == 0) {
+        const int64_t t_tok = row / p.H, h = row - t_tok * p.H;
+        p.mean_out[h * p.head_stride_rows + t_tok] = mean;
+      }
+    }
+  }
+  __shared__ uint32_t red[8];
+  m = warp_max_u32(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+    v = warp_max_u32(v);
+    if (threadIdx.x == 0) p.partials_w[blockIdx.x] = v;
   }
 }
 
@@ -302,8 +412,7 @@ __global__ void __launch_bounds__(256) quant_kernel(const __grid_constant__ Quan
 // cooperative persistent grid, one CTA per SM.  Each CTA bulk-copies (TMA engine, one
 // cp.async.bulk per tensor) its contiguous slice of K and of V -- 194 KB per SM for the Wan chunk --
 // into shared memory, so HBM is read exactly once.  Per tensor: local amax from smem -> partial ->
-// grid barrier (monotonic counter, no reset) -> every CTA reduces the partials to g -> quantizes its
-// slice from smem.  K is quantized while V is still landing.
+// grid barrier (tagged slots, no reset) -> g -> quantize the slice from smem.
 #ifndef KVQ_QUANT_THREADS
 #define KVQ_QUANT_THREADS 512
 #endif
@@ -340,6 +449,40 @@ KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
   return m;
 }
 
+// K-smoothing in the single-pass kernel: row means of the smem K slice (stored to smem and to the
+// cache's mean slot) and the slice max of |K_bar|.  Block i of the slice belongs to local row
+// i / kNB; the slice starts on a row boundary, so the kNB blocks of a row sit in kNB consecutive
+// lanes of one warp.
+template <int DT, int D>
+KVQ_DEV uint32_t smem_smooth_absmax(const QuantParams& p, const uint8_t* s, int nu, int64_t u0, float* s_mean) {
+  constexpr int kNB = D / 16;
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
+  const int tid = threadIdx.x;
+  uint32_t m = 0;
+  for (int base = tid & ~31; base < nu; base += kFusedThreads) {
+    const int i = base + (tid & 31);
+    const bool valid = i < nu;
+    float v[16];
+    if (valid) {
+      unpack_block16<DT>(s + (size_t)i * kUB, v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
+    }
+    const float mean = row_mean<kNB>(v);
+    if (valid) {
+      m = max(m, smoothed_absmax_bits(v, mean));
+      if (i % kNB == 0) {
+        s_mean[i / kNB] = mean;
+        const int64_t row = (u0 + i) / kNB;
+        const int64_t t_tok = row / p.H, h = row - t_tok * p.H;
+        p.mean_out[h * p.head_stride_rows + t_tok] = mean;
+      }
+    }
+  }
+  return m;
+}
+
 // debug timeline (globaltimer ns) of CTA 0 (slots 0-7) and the last CTA (8-15) when p.trace is set
 #define QTRACE(ev)                                                                       \
   do {                                                                                   \
@@ -352,10 +495,13 @@ KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
 
 // STAGED = true: the single-pass cooperative kernel described above.  STAGED = false: the second
 // pass of the two-launch path -- same per-block work, data read from global memory (L2-resident
-// after the amax pass), tensor amax reduced from the amax kernel's partials, ordinary launch.
-template <int DT, int D, bool STAGED>
+// after the amax pass), tensor amax reduced from the amax kernels' partials, ordinary launch.
+// MODE: kModeSearch (Four-Over-Six for K and V), kModeSmoothK (K-smoothing of K).
+template <int DT, int D, bool STAGED, int MODE>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     quant_fused_kernel(const __grid_constant__ QuantParams p, unsigned long long* slots, int upc) {
+  constexpr bool SEARCH = (MODE & kModeSearch) != 0;
+  constexpr bool SMOOTH = (MODE & kModeSmoothK) != 0;
   const unsigned long long epoch = p.epoch;
   constexpr int kNB = D / 16;
   constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);  // bytes per 16-element block
@@ -370,8 +516,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int64_t left = NU - u0;
   const int nu = left <= 0 ? 0 : (left < upc ? (int)left : upc);
   const uint32_t slice = (uint32_t)upc * kUB;  // the V slice follows the K slice in smem
-  // flagged block indices [upc]
+  // flagged block indices [upc], then (single pass, smoothing) the K row means [upc / kNB]
   uint32_t* queue = reinterpret_cast<uint32_t*>(STAGED ? sm + 2 * (size_t)slice : sm);
+  float* s_mean = reinterpret_cast<float*>(queue + upc);
   if (tid < 2) s_am[tid] = 0;
   if (tid == 0) {
     s_nq = 0;
@@ -380,8 +527,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  // K is requested first; V (KVQ_QUANT_V_DELAY) only once this CTA's K slice has landed, so the
-  // grid's K reads finish early and K's amax + quantization overlap V's landing.
+  // K is requested first; V (KVQ_QUANT_V_DELAY) only once this CTA's K slice has landed.
   auto issue = [&](int t) {
     mbar_arrive_expect_tx(bar + t, (uint32_t)nu * kUB);
     bulk_g2s(sm + t * slice, (const uint8_t*)p.x[t] + u0 * kUB, (uint32_t)nu * kUB, bar + t);
@@ -405,7 +551,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if (nu > 0) mbar_wait(bar + t, 0);
       if (t == 0 && kVDelay && tid == 0 && nu > 0) issue(1);
       QTRACE(t == 0 ? 1 : 5);
-      const uint32_t lm = warp_max_u32(smem_absmax<DT>(sm + t * slice, nu * kUB));
+      const uint32_t lm = warp_max_u32(SMOOTH && t == 0 ? smem_smooth_absmax<DT, D>(p, sm, nu, u0, s_mean)
+                                                        : smem_absmax<DT>(sm + t * slice, nu * kUB));
       if ((tid & 31) == 0) red2[t][tid >> 5] = lm;
       __syncthreads();
       if (tid == 0) {
@@ -416,14 +563,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
     }
   } else if (p.ext_amax) {
+    // caller-supplied amax (Ulysses); with smoothing the caller's K amax is of K_bar, and the row
+    // means are computed here
     if (STAGED && nu > 0) {
       mbar_wait(bar + 0, 0);
       if (kVDelay && tid == 0) issue(1);
-      mbar_wait(bar + 1, 0);
     }
+    if (SMOOTH) {
+      if (STAGED) (void)smem_smooth_absmax<DT, D>(p, sm, nu, u0, s_mean);
+    }
+    if (STAGED && nu > 0) mbar_wait(bar + 1, 0);
     if (tid < 2) s_am[tid] = __float_as_uint(p.ext_amax[tid]) & 0x7FFFFFFFu;
     __syncthreads();
-  } else {  // two-pass: reduce the amax kernel's per-CTA partials
+  } else {  // two-pass: reduce the amax kernels' per-CTA partials
     uint32_t mk = 0, mv = 0;
     for (int k = tid; k < kNumPartials; k += kFusedThreads) {
       mk = max(mk, p.partials[k]);
@@ -439,6 +591,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   }
   unsigned long long pre = 0;  // V slot loaded ahead (tid < G), checked after K is quantized
   for (int t = 0; t < 2; ++t) {
+    const bool smooth_t = SMOOTH && t == 0;
     if (STAGED && p.ext_amax == nullptr) {  // wait for every CTA's slot of tensor t
       uint32_t m = 0;
       for (int k = tid; k < G; k += kFusedThreads) {
@@ -480,66 +633,49 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // two blocks per thread per iteration (independent streams for latency hiding)
     for (int i = tid; i < nu; i += kQNB * kFusedThreads) {
       int ib[kQNB];
+      int64_t orow[kQNB];
 #pragma unroll
       for (int b = 0; b < kQNB; ++b) ib[b] = i + b * kFusedThreads < nu ? i + b * kFusedThreads : i;
       float v[kQNB][16];
 #pragma unroll
       for (int b = 0; b < kQNB; ++b) {
-        const uint8_t* src = s + (size_t)ib[b] * kUB;
-        if (DT == DT_BF16) {
-          const uint4 x0 = *reinterpret_cast<const uint4*>(src), x1 = *reinterpret_cast<const uint4*>(src + 16);
-          const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            v[b][2 * k] = __uint_as_float(w[k] << 16);
-            v[b][2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4 x = reinterpret_cast<const float4*>(src)[k];
-            v[b][4 * k] = x.x; v[b][4 * k + 1] = x.y; v[b][4 * k + 2] = x.z; v[b][4 * k + 3] = x.w;
-          }
-        }
+        const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
+        const uint32_t row = u / kNB;
+        const uint32_t t_tok = div_small(row, (uint32_t)p.H, invH);
+        orow[b] = (int64_t)(row - t_tok * (uint32_t)p.H) * p.head_stride_rows + t_tok;
+        unpack_block16<DT>(s + (size_t)ib[b] * kUB, v[b]);
+        if (smooth_t) subtract_mean(v[b], STAGED ? s_mean[ib[b] / kNB] : p.mean_out[orow[b]]);
       }
       uint32_t sb[kQNB], w0[kQNB], w1[kQNB];
-      const uint32_t flags = quantize_blocks_fast<kQNB>(v, g, rg, sb, w0, w1) | all_exact;
+      const uint32_t flags = quantize_blocks_fast<kQNB, SEARCH>(v, g, rg, sb, w0, w1) | all_exact;
 #pragma unroll
       for (int b = 0; b < kQNB; ++b) {
         if (b > 0 && ib[b] == ib[0]) break;
         if (flags & (1u << b)) queue[atomicAdd(&s_nq, 1)] = (uint32_t)ib[b];  // exact recompute below
-        const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
-        const uint32_t row = u / kNB;
-        const int j = (int)(u - row * kNB);
-        const uint32_t t_tok = div_small(row, (uint32_t)p.H, invH);
-        const uint32_t h = row - t_tok * (uint32_t)p.H;
-        const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
-        *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(w0[b], w1[b]);
-        scales[orow * kNB + j] = (uint8_t)sb[b];
+        const int j = (int)(((uint32_t)u0 + (uint32_t)ib[b]) % kNB);
+        *reinterpret_cast<uint2*>(codes + orow[b] * (D / 2) + j * 8) = make_uint2(w0[b], w1[b]);
+        scales[orow[b] * kNB + j] = (uint8_t)sb[b];
       }
     }
     __syncthreads();
     if (t == 0) QTRACE(4);
-    // deferred exact path for the flagged blocks (a few % of blocks; one thread per block)
+    // deferred exact path for flagged blocks (out-of-range scales only; one thread per block)
     const int nq = s_nq;
     for (int e = tid; e < nq; e += kFusedThreads) {
       const int ibk = (int)queue[e];
-      float v[16];
-      const uint8_t* src = s + (size_t)ibk * kUB;
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        v[k] = DT == DT_BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
-                             : reinterpret_cast<const float*>(src)[k];
-      uint32_t sbe, a, bb;
-      quantize_block16_exact(v, g, sbe, a, bb);
       const uint32_t u = (uint32_t)u0 + (uint32_t)ibk;
       const uint32_t row = u / kNB;
       const int j = (int)(u - row * kNB);
       const uint32_t t_tok = row / (uint32_t)p.H;
       const uint32_t h = row - t_tok * (uint32_t)p.H;
-      const int64_t orow = (int64_t)h * p.head_stride_rows + t_tok;
-      *reinterpret_cast<uint2*>(codes + orow * (D / 2) + j * 8) = make_uint2(a, bb);
-      scales[orow * kNB + j] = (uint8_t)sbe;
+      const int64_t orw = (int64_t)h * p.head_stride_rows + t_tok;
+      float v[16];
+      unpack_block16<DT>(s + (size_t)ibk * kUB, v);
+      if (smooth_t) subtract_mean(v, STAGED ? s_mean[ibk / kNB] : p.mean_out[orw]);
+      uint32_t sbe, a, bb;
+      quantize_block16_exact<SEARCH>(v, g, sbe, a, bb);
+      *reinterpret_cast<uint2*>(codes + orw * (D / 2) + j * 8) = make_uint2(a, bb);
+      scales[orw * kNB + j] = (uint8_t)sbe;
     }
     __syncthreads();
     if (tid == 0) s_nq = 0;
@@ -549,7 +685,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #undef QTRACE
 
 // Eq. 2: x^ = dec(c) dec(s) g.  dec(c) dec(s) is exact in fp32 (<= 7 significant
-// bits), so one __fmul_rn by g gives RN32 of the exact product.
+// bits), so one FMA with g (and the K-smoothing row mean, else 0) rounds the exact value once.
 template <int D>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DequantParams p) {
   constexpr int kNB = D / 16;
@@ -563,6 +699,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ De
     const int64_t srow = (int64_t)h * p.head_stride_rows + t;
     const uint2 c = *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
     const float s = e4m3_to_f32(p.scales[tsr][srow * kNB + j]);
+    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : 0.0f;  // K-smoothing restitution (reading Z20)
     float o[16];
     uint32_t cw[2] = {c.x, c.y};
 #pragma unroll
@@ -570,8 +707,8 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ De
       uint32_t h2 = f16x2_from_e2m1x2((cw[k >> 2] >> (8 * (k & 3))) & 0xFF);
       float lo = __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFF)));
       float hi = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
-      o[2 * k] = __fmul_rn(__fmul_rn(lo, s), g);
-      o[2 * k + 1] = __fmul_rn(__fmul_rn(hi, s), g);
+      o[2 * k] = __fmaf_rn(__fmul_rn(lo, s), g, m);      // RN32(dec(c) dec(s) g + mean), one rounding
+      o[2 * k + 1] = __fmaf_rn(__fmul_rn(hi, s), g, m);
     }
     if (p.out_dtype == DT_FP32) {
       float4* dst = reinterpret_cast<float4*>((float*)p.out[tsr] + row * D + j * 16);
@@ -595,16 +732,20 @@ template <int D>
 __global__ void __launch_bounds__(256) export_kernel(const __grid_constant__ ExportParams p) {
   constexpr int kNB = D / 16;
   const int tsr = blockIdx.y;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *p.g_out[tsr] = p.g[tsr];
+  const bool bytes = p.codes_out[tsr] != nullptr;  // false: K-smoothing means only
+  if (bytes && blockIdx.x == 0 && threadIdx.x == 0) *p.g_out[tsr] = p.g[tsr];
   const int64_t total = (int64_t)p.T * p.H * kNB;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < total; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = b / kNB;
     const int j = (int)(b - row * kNB);
     const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
     const int64_t srow = (int64_t)h * p.head_stride_rows + t;
-    *reinterpret_cast<uint2*>(p.codes_out[tsr] + row * (D / 2) + j * 8) =
-        *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
-    p.scales_out[tsr][row * kNB + j] = p.scales[tsr][srow * kNB + j];
+    if (bytes) {
+      *reinterpret_cast<uint2*>(p.codes_out[tsr] + row * (D / 2) + j * 8) =
+          *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
+      p.scales_out[tsr][row * kNB + j] = p.scales[tsr][srow * kNB + j];
+    }
+    if (tsr == 0 && j == 0 && p.mean && p.mean_out) p.mean_out[row] = p.mean[srow];
   }
 }
 
@@ -635,13 +776,14 @@ __global__ void __launch_bounds__(256) dequant_window_kernel(const __grid_consta
     const float g = gtab[ws.seg[s].slot * 2 + tsr];
     const uint2 c = *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
     const float sc = e4m3_to_f32(p.scales[tsr][srow * kNB + j]);
+    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : 0.0f;
     uint32_t cw[2] = {c.x, c.y}, w[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t h2 = f16x2_from_e2m1x2((cw[k >> 2] >> (8 * (k & 3))) & 0xFF);
       float lo = __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFF)));
       float hi = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__fmul_rn(lo, sc), g), __fmul_rn(__fmul_rn(hi, sc), g));
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmaf_rn(__fmul_rn(lo, sc), g, m), __fmaf_rn(__fmul_rn(hi, sc), g, m));
       w[k] = *reinterpret_cast<uint32_t*>(&b2);
     }
     uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.out[tsr] + row * D + j * 16);
@@ -679,40 +821,39 @@ int grid_for(int64_t work, int per_cta) {
 }  // namespace
 
 cudaError_t launch_amax(const void* K, const void* V, int dtype, int64_t n, uint32_t* partials, DevStatus* status,
-                        cudaStream_t st) {
-  dim3 grid(kNumPartials, 2);
+                        cudaStream_t st, int tsr_begin) {
+  dim3 grid(kNumPartials, 2 - tsr_begin);
   if (dtype == DT_BF16)
-    amax_kernel<DT_BF16><<<grid, 256, 0, st>>>(K, V, n, partials, status);
+    amax_kernel<DT_BF16><<<grid, 256, 0, st>>>(K, V, n, partials, status, tsr_begin);
   else
-    amax_kernel<DT_FP32><<<grid, 256, 0, st>>>(K, V, n, partials, status);
+    amax_kernel<DT_FP32><<<grid, 256, 0, st>>>(K, V, n, partials, status, tsr_begin);
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize(const QuantParams& p, cudaStream_t st) {
-  const int64_t blocks = (int64_t)p.rows * (p.d / 16);
-  dim3 grid(grid_for(blocks, 256), 2);
+cudaError_t launch_smooth_amax(const QuantParams& p, cudaStream_t st) {
   if (p.dtype == DT_BF16) {
-    if (p.d == 128) quant_kernel<DT_BF16, 128><<<grid, 256, 0, st>>>(p);
-    else quant_kernel<DT_BF16, 64><<<grid, 256, 0, st>>>(p);
+    if (p.d == 128) smooth_amax_kernel<DT_BF16, 128><<<kNumPartials, 256, 0, st>>>(p);
+    else smooth_amax_kernel<DT_BF16, 64><<<kNumPartials, 256, 0, st>>>(p);
   } else {
-    if (p.d == 128) quant_kernel<DT_FP32, 128><<<grid, 256, 0, st>>>(p);
-    else quant_kernel<DT_FP32, 64><<<grid, 256, 0, st>>>(p);
+    if (p.d == 128) smooth_amax_kernel<DT_FP32, 128><<<kNumPartials, 256, 0, st>>>(p);
+    else smooth_amax_kernel<DT_FP32, 64><<<kNumPartials, 256, 0, st>>>(p);
   }
   return cudaGetLastError();
 }
 
-template <int DT, int D>
-cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,
-                           cudaStream_t st) {
+template <int DT, int D, int MODE>
+cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, int sms, cudaStream_t st) {
   constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
   const int64_t NU = (int64_t)p.rows * (D / 16);
   int upc = (int)((NU + sms - 1) / sms);
   if (upc < 64) upc = 64;
   upc = (upc + 7) & ~7;  // 128-byte aligned V slice
   const int G = (int)((NU + upc - 1) / upc);
-  const size_t smem = (size_t)2 * upc * kUB + (size_t)upc * sizeof(uint32_t);  // K, V slices + flag queue
+  // K, V slices + flag queue (+ K row means with smoothing)
+  const size_t smem = (size_t)2 * upc * kUB + (size_t)upc * sizeof(uint32_t) +
+                      ((MODE & kModeSmoothK) ? (size_t)(upc / (D / 16)) * sizeof(float) : 0);
   if (smem > 220 * 1024 || G > kNumPartials || G > kMaxFusedCtas) return cudaErrorNotSupported;
-  auto kern = quant_fused_kernel<DT, D, true>;
+  auto kern = quant_fused_kernel<DT, D, true, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -725,40 +866,59 @@ cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, u
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  (void)partials;
-  // counters -> the barrier slots: [G][2] x u64 (tag << 32 | amax bits) for K and V
+  // counters -> the barrier slots: [G] lines of kSlotU64 u64, (tag << 32 | amax bits) for K and V
   return cudaLaunchKernelEx(&cfg, kern, p, counters, upc);
 }
 
-// second pass of the two-launch path (after launch_amax): per-block work as in the single-pass kernel
-template <int DT, int D>
+// second pass of the two-launch path (after the amax pass): per-block work as in the single-pass kernel
+template <int DT, int D, int MODE>
 cudaError_t launch_quant2_t(const QuantParams& p, int sms, cudaStream_t st) {
   const int64_t NU = (int64_t)p.rows * (D / 16);
   int64_t G = sms;
   if ((NU + G - 1) / G > 8192) G = (NU + 8191) / 8192;  // flag queue <= 32 KB of smem
-  const int upc = (int)((NU + G - 1) / G);
+  int upc = (int)((NU + G - 1) / G);
+  upc = (upc + 7) & ~7;  // slices start on row boundaries
   G = (NU + upc - 1) / upc;
   const size_t smem = (size_t)upc * sizeof(uint32_t);
-  auto kern = quant_fused_kernel<DT, D, false>;
+  auto kern = quant_fused_kernel<DT, D, false, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)G, kFusedThreads, smem, st>>>(p, nullptr, upc);
   return cudaGetLastError();
 }
 
+template <int DT, int D>
+cudaError_t quant2_mode(const QuantParams& p, int sms, cudaStream_t st) {
+  switch (p.mode & 3) {
+    case 0: return launch_quant2_t<DT, D, 0>(p, sms, st);
+    case 1: return launch_quant2_t<DT, D, 1>(p, sms, st);
+    case 2: return launch_quant2_t<DT, D, 2>(p, sms, st);
+    default: return launch_quant2_t<DT, D, 3>(p, sms, st);
+  }
+}
+
+template <int DT, int D>
+cudaError_t fused_mode(const QuantParams& p, unsigned long long* counters, int sms, cudaStream_t st) {
+  switch (p.mode & 3) {
+    case 0: return launch_fused_t<DT, D, 0>(p, counters, sms, st);
+    case 1: return launch_fused_t<DT, D, 1>(p, counters, sms, st);
+    case 2: return launch_fused_t<DT, D, 2>(p, counters, sms, st);
+    default: return launch_fused_t<DT, D, 3>(p, counters, sms, st);
+  }
+}
+
 cudaError_t launch_quantize2(const QuantParams& p, int sms, cudaStream_t st) {
   if (p.dtype == DT_BF16)
-    return p.d == 128 ? launch_quant2_t<DT_BF16, 128>(p, sms, st) : launch_quant2_t<DT_BF16, 64>(p, sms, st);
-  return p.d == 128 ? launch_quant2_t<DT_FP32, 128>(p, sms, st) : launch_quant2_t<DT_FP32, 64>(p, sms, st);
+    return p.d == 128 ? quant2_mode<DT_BF16, 128>(p, sms, st) : quant2_mode<DT_BF16, 64>(p, sms, st);
+  return p.d == 128 ? quant2_mode<DT_FP32, 128>(p, sms, st) : quant2_mode<DT_FP32, 64>(p, sms, st);
 }
 
 cudaError_t launch_quantize_fused(const QuantParams& p, unsigned long long* counters, uint32_t* partials, int sms,
                                   cudaStream_t st) {
+  (void)partials;
   if (p.dtype == DT_BF16)
-    return p.d == 128 ? launch_fused_t<DT_BF16, 128>(p, counters, partials, sms, st)
-                      : launch_fused_t<DT_BF16, 64>(p, counters, partials, sms, st);
-  return p.d == 128 ? launch_fused_t<DT_FP32, 128>(p, counters, partials, sms, st)
-                    : launch_fused_t<DT_FP32, 64>(p, counters, partials, sms, st);
+    return p.d == 128 ? fused_mode<DT_BF16, 128>(p, counters, sms, st) : fused_mode<DT_BF16, 64>(p, counters, sms, st);
+  return p.d == 128 ? fused_mode<DT_FP32, 128>(p, counters, sms, st) : fused_mode<DT_FP32, 64>(p, counters, sms, st);
 }
 
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t st) {

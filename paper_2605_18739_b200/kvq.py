@@ -68,6 +68,7 @@ _SIGS = {
                                        _P, ctypes.c_int, _P]),
     "kv_dequantize": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P]),
     "kv_export_chunk": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "kv_export_kmean": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P]),
     "kvq_resident_bytes": (ctypes.c_size_t, [_P]),
     "kvq_resident_chunks": (ctypes.c_int32, [_P, ctypes.c_int32]),
     "kv_dequantize_window": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(_Mask), _P, _P,
@@ -140,11 +141,15 @@ class KVCache:
     """Chunkwise NVFP4 KV cache of one rank over a torch-owned arena."""
 
     def __init__(self, num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk,
-                 sink_frames=0, window_frames=None, max_chunk_slots=8, device=None):
+                 sink_frames=0, window_frames=None, max_chunk_slots=8, device=None,
+                 scale_search=False, k_smoothing=False):
+        """scale_search: Four-Over-Six block scales for K and V (PAPER.md:146, 728-739);
+        k_smoothing: keys stored mean-centred per (t, h), means restored."""
         L = lib()
         window_frames = window_frames if window_frames is not None else max_chunk_slots * frames_per_chunk
         self.cfg = Config(num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk, sink_frames,
-                          window_frames, max_chunk_slots, 0, 0)
+                          window_frames, max_chunk_slots, 1 if scale_search else 0, 1 if k_smoothing else 0)
+        self.scale_search, self.k_smoothing = bool(scale_search), bool(k_smoothing)
         nbytes = L.kvq_cache_bytes(ctypes.byref(self.cfg))
         if nbytes == 0:
             raise KVQError(-1, "kvq_cache_bytes (bad config)")
@@ -219,6 +224,12 @@ class KVCache:
         _check(lib().kv_export_chunk(self._h, layer, chunk_index, _ptr(out["codes_k"]), _ptr(out["scales_k"]),
                                      _ptr(out["g_k"]), _ptr(out["codes_v"]), _ptr(out["scales_v"]), _ptr(out["g_v"]),
                                      _stream()), "kv_export_chunk")
+        return out
+
+    def export_kmean(self, layer, chunk_index):
+        """K-smoothing row means of a resident chunk, fp32 [T_c*H] (t, h) t-major."""
+        out = torch.empty(self.T_c * self.H, dtype=torch.float32, device=self.device)
+        _check(lib().kv_export_kmean(self._h, layer, chunk_index, _ptr(out), _stream()), "kv_export_kmean")
         return out
 
     def n_keys(self, layer, mask: Mask):

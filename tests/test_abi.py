@@ -75,9 +75,14 @@ def test_cache_bytes_and_validation(lib):
     assert payload + attn_ws <= n <= payload + attn_ws + 64 * 1024
     # NVFP4 resident bytes vs bf16 for 8 slots x 30 layers (1.94 GB vs 6.90 GB)
     assert abs(30 * 12 * 8 * 4680 * 72 * 2 / 1e9 - 1.94) < 0.01
-    for bad in (Config(30, 12, 96, 1560, 3, 3, 21, 8, 0, 0), Config(30, 12, 128, 1560, 3, 3, 21, 8, 1, 0),
-                Config(30, 12, 128, 1560, 3, 3, 21, 0, 0, 0), Config(0, 12, 128, 1560, 3, 3, 21, 8, 0, 0)):
+    for bad in (Config(30, 12, 96, 1560, 3, 3, 21, 8, 0, 0), Config(30, 12, 128, 1560, 3, 3, 21, 8, 2, 0),
+                Config(30, 12, 128, 1560, 3, 3, 21, 8, 0, 2), Config(30, 12, 128, 1560, 3, 3, 21, 0, 0, 0),
+                Config(0, 12, 128, 1560, 3, 3, 21, 8, 0, 0)):
         assert lib.kvq_cache_bytes(ctypes.byref(bad)) == 0
+    # Four-Over-Six needs no extra bytes; K-smoothing adds one fp32 mean per cached K row
+    assert lib.kvq_cache_bytes(ctypes.byref(Config(30, 12, 128, 1560, 3, 3, 21, 8, 1, 0))) == n
+    ns = lib.kvq_cache_bytes(ctypes.byref(Config(30, 12, 128, 1560, 3, 3, 21, 8, 1, 1)))
+    assert n + 30 * 12 * 8 * T_pad * 4 <= ns <= n + 30 * 12 * 8 * T_pad * 4 + 4096
 
 
 def test_strerror(lib):
