@@ -339,7 +339,9 @@ def dequantize_kv_chunk_rn32(q, T, H, d):
     codes = unpack_codes(q["codes"])
     rows = T * H
     v = (e2m1_decode(codes).reshape(rows, d // BLOCK, BLOCK) * e4m3_decode(q["scales"])[..., None]).reshape(rows, d)
-    mean = np.asarray(q["mean"], dtype=np.float64)[:, None] if "mean" in q else np.zeros((rows, 1))
+    # without a mean the addend is -0.0, the additive identity: RN32(v g + -0) = RN32(v g) keeps Eq. 2's
+    # sign of zero (code 0x8 decodes to -0.0 * s * g = -0.0, reading Z6)
+    mean = np.asarray(q["mean"], dtype=np.float64)[:, None] if "mean" in q else np.full((rows, 1), -0.0)
     return _rn32_fma(v, q["g"], mean).reshape(T, H, d)
 
 

@@ -10,8 +10,9 @@
 // Numerics: K^' = dec(code) * dec(s) and V^' likewise are EXACT in fp16, so the
 // tensor cores see the exact quantized lattice; the FP32 tensor scales g_K, g_V are applied in
 // fp32 outside the MMA (g_K in the exponent scale, g_V folded into the O rescale factor).
-// Q is rounded once to fp16, P is fp16, accumulation is fp32 in TMEM, the running max is exact
-// (no lazy threshold), l is summed in fp32 from the fp16-rounded P.
+// bf16 Q is exact in fp16; fp32 Q is split into fp16 hi + lo (QSPLIT).  P is fp16, accumulation is
+// fp32 in TMEM, the running max is lazy (moves only when a tile exceeds it by 2^kLazyLog2), and l is
+// summed in fp32 from the fp16-rounded P.
 //
 // Structure: one CTA = one head x two 128-query tiles (256 rows share every dequantized KV
 // tile), warp-specialized, 13 warps:
@@ -54,19 +55,31 @@ KVQ_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::
 template <int N>
 KVQ_DEV void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
-template <int D>
+// QSPLIT (fp32 Q): Q = Q_hi + Q_lo, both fp16, and S = Q_hi K^T + Q_lo K^T accumulate in TMEM, so
+// fp32 queries lose ~2^-22 instead of fp16's 2^-11 (the single rounding costs up to 5e-3 max-abs on
+// peaked rows with large key offsets).  The two Q_lo tiles take the second K/V buffers at d = 128
+// (single-buffered K/V; the fp32-Q mode is the parity configuration, not the bench one) and two extra
+// tiles at d = 64.
+template <int D, bool QSPLIT = false>
 struct WsSmem {
   static constexpr int kTile = 128 * D * 2;
+  static constexpr int kNBuf = (QSPLIT && D == 128) ? 1 : 2;  // K^/V^ buffers
   static constexpr int kQ0 = 0;
   static constexpr int kQ1 = kTile;
   static constexpr int kK0 = 2 * kTile;
   static constexpr int kK1 = 3 * kTile;
   static constexpr int kV0 = 4 * kTile;
   static constexpr int kV1 = 5 * kTile;
-  static constexpr int kBar = 6 * kTile;
+  static constexpr int kQL0 = D == 128 ? 3 * kTile : 6 * kTile;  // QSPLIT only
+  static constexpr int kQL1 = D == 128 ? 5 * kTile : 7 * kTile;
+  static constexpr int kBar = (QSPLIT && D != 128) ? 8 * kTile : 6 * kTile;
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
   static constexpr int kMean = kBar + 16 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
   static constexpr int kBytes = kMean + 2 * 2 * 128 * 4 + 1024;
+  // K^/V^ buffer of global tile g, and the mbarrier parities of its full / empty waits
+  static KVQ_DEV int buf(int g) { return kNBuf == 2 ? (g & 1) : 0; }
+  static KVQ_DEV uint32_t full_par(int g) { return kNBuf == 2 ? ((g >> 1) & 1) : (g & 1); }
+  static KVQ_DEV uint32_t empty_par(int g) { return kNBuf == 2 ? (((g >> 1) - 1) & 1) : ((g - 1) & 1); }
 };
 
 // address of 16-byte chunk c (8 consecutive elements along d) of row r in a 128-row tile
@@ -133,16 +146,19 @@ KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool val
 }
 
 // Q row -> fp16 (bf16 in bf16-KV mode) into a tile row.  SUM: also returns sum_u Q_iu of the
-// rounded values (fp32; the K-smoothing restitution term, see attn_ws_kernel).
-template <int D, bool MMA_BF16, bool SUM = false>
-KVQ_DEV float load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64_t row_index, bool valid) {
+// rounded values (fp32; the K-smoothing restitution term, see attn_ws_kernel).  QSPLIT (fp32 Q):
+// hi = RN16(q) into the tile, lo = RN16(q - hi) (q - hi is exact in fp32) into the lo tile, and the
+// sum is over hi + lo.
+template <int D, bool MMA_BF16, bool SUM = false, bool QSPLIT = false>
+KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, int q_dtype, int64_t row_index,
+                         bool valid) {
   float qsum = 0.0f;
 #pragma unroll
   for (int c = 0; c < D / 8; ++c) {
-    uint32_t o[4] = {0, 0, 0, 0};
+    uint32_t o[4] = {0, 0, 0, 0}, ol[4] = {0, 0, 0, 0};
     if (valid) {
       float f[8];
-      if (q_dtype == DT_BF16) {
+      if (!QSPLIT && q_dtype == DT_BF16) {
         uint4 v = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)Q + row_index * D) + c);
         if (MMA_BF16) {
           o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
@@ -156,11 +172,17 @@ KVQ_DEV float load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64
         float4 a = __ldg(src), b = __ldg(src + 1);
         f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
           o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
+          if (QSPLIT) {
+            const float2 h2 = __half22float2(*reinterpret_cast<const __half2*>(&o[k]));
+            ol[k] = pack_half2(f[2 * k] - h2.x, f[2 * k + 1] - h2.y);
+            if (SUM) qsum += f[2 * k] + f[2 * k + 1];
+          }
+        }
       }
     }
-    if (SUM) {
+    if (SUM && !QSPLIT) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&o[k]));
@@ -168,6 +190,7 @@ KVQ_DEV float load_q_row(uint32_t base, int r, const void* Q, int q_dtype, int64
       }
     }
     st_shared_v4(chunk_addr(base, r, c), o[0], o[1], o[2], o[3]);
+    if (QSPLIT) st_shared_v4(chunk_addr(base_lo, r, c), ol[0], ol[1], ol[2], ol[3]);
   }
   return qsum;
 }
@@ -253,9 +276,9 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
 // and the score is restored exactly as q.k = q.k_bar + m_j sum_u q_u -- a rank-1 term added in
 // fp32 to the scaled MMA scores before the row max, from the fp32 row sum of the (rounded) Q row
 // and the key means of the tile (one coalesced load per softmax thread, shared through smem).
-template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH>
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH, bool QSPLIT>
 __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
-  using SM = WsSmem<D>;
+  using SM = WsSmem<D, QSPLIT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // tile bases: Q_i = sbase + i*T, K_b = sbase + (2+b)*T, V_b = sbase + (4+b)*T
@@ -264,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #define SQ(i) (sbase + (uint32_t)(i) * kT)
 #define SK(b) (sbase + (2u + (uint32_t)(b)) * kT)
 #define SV(b) (sbase + (4u + (uint32_t)(b)) * kT)
+#define SQL(i) (sbase + (uint32_t)((i) ? SM::kQL1 : SM::kQL0))
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
   uint64_t* kfull = bars + 0;   // [2] dequant -> MMA, per K^ buffer
   uint64_t* vfull = bars + 2;   // [2]
@@ -313,7 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
-      const float qsum = load_q_row<D, MMA_BF16, SMOOTH>(SQ(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      const float qsum = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
+                                                                 (int64_t)t * H + h, t < p.Tq);
       const uint64_t qsb2 = f32x2_pack(qsum * p.scale_log2, qsum * p.scale_log2);
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
@@ -515,19 +540,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       tile_seek(p, pc.tb, it);
       for (int j = pc.tb; j < pc.te; ++j, ++g, tile_next(p, it)) {
         const AttnSeg& sg = p.seg[it.seg];
-        const int b = g & 1;
-        const uint32_t par = ((g >> 1) - 1) & 1;
+        const int b = SM::buf(g);
+        const uint32_t par = SM::empty_par(g);
         if (NVFP4) {
           const int64_t crow = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
           PackedRow<D> pk, pv;
           load_packed_row<D>(pk, p.codes_k + crow * (D / 2), p.scales_k + crow * (D / 16));
           load_packed_row<D>(pv, p.codes_v + crow * (D / 2), p.scales_v + crow * (D / 16));
-          if (g >= 2) mbar_wait(kempty + b, par);
+          if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
           store_dequant_row<D>(SK(b), r, pk);
           fence_proxy_async_smem();
           mbar_arrive(kfull + b);
           if (r == 0) KVQ_TRACE(g, 6);
-          if (g >= 2) mbar_wait(vempty + b, par);
+          if (g >= SM::kNBuf) mbar_wait(vempty + b, par);
           store_dequant_row<D>(SV(b), r, pv);
           fence_proxy_async_smem();
           mbar_arrive(vfull + b);
@@ -536,11 +561,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           const int key = it.t0 + r;
           const bool valid = key < sg.end;
           const int64_t off = valid ? ((int64_t)key * H + h) * D * 2 : 0;
-          if (g >= 2) mbar_wait(kempty + b, par);
+          if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
           copy_row_to_smem<D>(SK(b), r, (const uint8_t*)p.Kb + off, valid);
           fence_proxy_async_smem();
           mbar_arrive(kfull + b);
-          if (g >= 2) mbar_wait(vempty + b, par);
+          if (g >= SM::kNBuf) mbar_wait(vempty + b, par);
           copy_row_to_smem<D>(SV(b), r, (const uint8_t*)p.Vb + off, valid);
           fence_proxy_async_smem();
           mbar_arrive(vfull + b);
@@ -558,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     constexpr uint32_t kIdS = umma_idesc_f16(128, 128, MMA_BF16 ? 1 : 0, 0, 0);
     constexpr uint32_t kIdO = umma_idesc_f16(128, D, MMA_BF16 ? 1 : 0, 0, 1);
     const uint64_t dQ0 = umma_desc_sw128(SQ(0), 16, 1024), dQ1 = umma_desc_sw128(SQ(1), 16, 1024);
+    const uint64_t dL0 = umma_desc_sw128(SQL(0), 16, 1024), dL1 = umma_desc_sw128(SQL(1), 16, 1024);
     const uint64_t dK0 = umma_desc_sw128(SK(0), 16, 1024), dK1 = umma_desc_sw128(SK(1), 16, 1024);
     const uint64_t dV0 = umma_desc_sw128(SV(0), 16384, 1024), dV1 = umma_desc_sw128(SV(1), 16384, 1024);
     auto issue_qk = [&](int qi, int b) {
@@ -568,6 +594,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
           umma_ss(dt, da + off, db + off, kIdS, kk > 0 ? 1u : 0u);
+        }
+        if (QSPLIT) {  // + Q_lo K^T into the same accumulator
+          const uint64_t dl = qi ? dL1 : dL0;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+            umma_ss(dt, dl + off, db + off, kIdS, 1u);
+          }
         }
       }
       __syncwarp();
@@ -592,22 +626,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       const int np = pc.te - pc.tb;
       mbar_wait(qfull + 0, k & 1);
       mbar_wait(qfull + 1, k & 1);
-      mbar_wait(kfull + (g & 1), (g >> 1) & 1);
+      mbar_wait(kfull + SM::buf(g), SM::full_par(g));
       tc_fence_after();
-      issue_qk(0, g & 1);
+      issue_qk(0, SM::buf(g));
       tc_commit(sfull + 0);
-      issue_qk(1, g & 1);
+      issue_qk(1, SM::buf(g));
       tc_commit(sfull + 1);
-      tc_commit(kempty + (g & 1));
+      tc_commit(kempty + SM::buf(g));
       for (int j = 0; j < np; ++j) {
-        const int gj = g + j, b = gj & 1, bn = (gj + 1) & 1;
-        mbar_wait(vfull + b, (gj >> 1) & 1);
+        const int gj = g + j, b = SM::buf(gj), bn = SM::buf(gj + 1);
+        mbar_wait(vfull + b, SM::full_par(gj));
         mbar_wait(pfull + 0, gj & 1);
         tc_fence_after();
         KVQ_TRACE(gj, 8);
         issue_pv(0, b, j == 0);
         if (j + 1 < np) {
-          mbar_wait(kfull + bn, ((gj + 1) >> 1) & 1);
+          mbar_wait(kfull + bn, SM::full_par(gj + 1));
           tc_fence_after();
           KVQ_TRACE(gj + 1, 9);
           issue_qk(0, bn);
@@ -638,6 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #undef SQ
 #undef SK
 #undef SV
+#undef SQL
 }
 
 // Merge the partial pieces of every split unit: O = sum_p 2^(m_p - m) O_p / sum_p 2^(m_p - m) l_p,
@@ -690,10 +725,10 @@ __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ At
   }
 }
 
-template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH = false>
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH = false, bool QSPLIT = false>
 cudaError_t launch_t(AttnParams p, cudaStream_t st) {
-  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16, SMOOTH>;
-  const int smem = WsSmem<D>::kBytes;
+  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16, SMOOTH, QSPLIT>;
+  const int smem = WsSmem<D, QSPLIT>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   p.qpairs = (p.Tq + 255) / 256;
@@ -720,12 +755,16 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int D, bool SMOOTH>
+cudaError_t launch_nvfp4(const AttnParams& p, cudaStream_t st) {
+  return p.q_dtype == DT_FP32 ? launch_t<D, true, false, SMOOTH, true>(p, st) : launch_t<D, true, false, SMOOTH>(p, st);
+}
+
 }  // namespace
 
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st) {
-  if (nvfp4_kv && p.mean_k)
-    return p.d == 128 ? launch_t<128, true, false, true>(p, st) : launch_t<64, true, false, true>(p, st);
-  if (nvfp4_kv) return p.d == 128 ? launch_t<128, true, false>(p, st) : launch_t<64, true, false>(p, st);
+  if (nvfp4_kv && p.mean_k) return p.d == 128 ? launch_nvfp4<128, true>(p, st) : launch_nvfp4<64, true>(p, st);
+  if (nvfp4_kv) return p.d == 128 ? launch_nvfp4<128, false>(p, st) : launch_nvfp4<64, false>(p, st);
   return p.d == 128 ? launch_t<128, false, true>(p, st) : launch_t<64, false, true>(p, st);
 }
 

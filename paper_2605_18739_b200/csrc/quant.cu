@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #undef QTRACE
 
 // Eq. 2: x^ = dec(c) dec(s) g.  dec(c) dec(s) is exact in fp32 (<= 7 significant
-// bits), so one FMA with g (and the K-smoothing row mean, else 0) rounds the exact value once.
+// bits), so one FMA with g (and the K-smoothing row mean, else -0) rounds the exact value once.
 template <int D>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DequantParams p) {
   constexpr int kNB = D / 16;
@@ -699,7 +699,9 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ De
     const int64_t srow = (int64_t)h * p.head_stride_rows + t;
     const uint2 c = *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
     const float s = e4m3_to_f32(p.scales[tsr][srow * kNB + j]);
-    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : 0.0f;  // K-smoothing restitution (reading Z20)
+    // K-smoothing restitution (reading Z20); else -0, the additive identity that keeps Eq. 2's
+    // sign of zero (code 0x8 -> -0.0, reading Z6)
+    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : -0.0f;
     float o[16];
     uint32_t cw[2] = {c.x, c.y};
 #pragma unroll
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(256) dequant_window_kernel(const __grid_consta
     const float g = gtab[ws.seg[s].slot * 2 + tsr];
     const uint2 c = *reinterpret_cast<const uint2*>(p.codes[tsr] + srow * (D / 2) + j * 8);
     const float sc = e4m3_to_f32(p.scales[tsr][srow * kNB + j]);
-    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : 0.0f;
+    const float m = (tsr == 0 && p.mean) ? p.mean[srow] : -0.0f;  // -0: keeps the sign of zero
     uint32_t cw[2] = {c.x, c.y}, w[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {

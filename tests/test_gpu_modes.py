@@ -20,6 +20,7 @@ from gpu_util import assert_chunk_bytes_equal, check_bf16_out, check_fp32_out
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
 MODES = [(True, False), (False, True), (True, True)]   # (scale_search, k_smoothing)
+ATT_MODES = [(False, False)] + MODES                    # attention: the plain path on the same keys too
 
 
 def _gpu():
@@ -146,7 +147,7 @@ def _run(T, H, d, tpf, fc, n_chunks, dtype, sink, window, slots, search, smooth,
     return c, o, qs
 
 
-@pytest.mark.parametrize("search,smooth", MODES)
+@pytest.mark.parametrize("search,smooth", ATT_MODES)
 @pytest.mark.parametrize("variant", ["iid", "peaked"])
 def test_modes_attention_tiny(search, smooth, variant):
     _gpu()
@@ -161,17 +162,23 @@ def test_modes_attention_tiny(search, smooth, variant):
         check_bf16_out(Ob, ref, O32)
 
 
-@pytest.mark.parametrize("search,smooth", MODES)
-def test_modes_attention_sink_window_ragged_d128(search, smooth):
-    # 3 tokens/frame x 50 -> ragged 150-token chunks; sink 1 frame, window 4 chunks
+@pytest.mark.parametrize("search,smooth", ATT_MODES)
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_modes_attention_sink_window_ragged_d128(search, smooth, dtype):
+    # 50 tokens/frame x 3 -> ragged 150-token chunks; sink 1 frame, window 12 frames (4 chunks); each
+    # chunk is attended right after its append (later appends evict the chunks an early mask reaches)
     _gpu()
     T, H, d, tpf, fc = 150, 3, 128, 50, 3
-    c, o, qs = _run(T, H, d, tpf, fc, 7, "bf16", 1, 12, 6, search, smooth)
-    for ch in (4, 6):
-        m = kvq.Mask(ch, 1, 12)
-        O32 = c.attention(0, qs[ch].torch(DEV), m, torch.float32).cpu().numpy()
-        ref = o.attend(0, ch, qs[ch].f64, 1, 12)
-        check_fp32_out(O32, ref)
+    c = _cache(H, d, tpf, fc, search, smooth, 1, 12, 6)
+    o = OracleKVCache(1, H, d, tpf, fc, scale_search=search, k_smoothing=smooth)
+    for ch in range(7):
+        q, k, v = _qkv(T, H, d, dtype, 0, ch, variant="peaked" if dtype == "fp32" else "iid")
+        c.append(0, ch, k.torch(DEV), v.torch(DEV))
+        o.append(0, ch, k.f64, v.f64)
+        if ch in (0, 4, 6):
+            m = kvq.Mask(ch, 1, 12)
+            O32 = c.attention(0, q.torch(DEV), m, torch.float32).cpu().numpy()
+            check_fp32_out(O32, o.attend(0, ch, q.f64, 1, 12))
 
 
 @pytest.fixture(scope="module")

@@ -227,6 +227,21 @@ def test_idempotence():
         assert g2 == g and np.array_equal(s2, s) and np.array_equal(c2, c)
 
 
+def test_dequant_fp32_keeps_sign_of_zero_and_is_idempotent():
+    # kv_dequantize's fp32 value RN32(dec(c) dec(s) g): Eq. 2 is a product, so code 0x8
+    # (-0, reading Z6) must come back as -0.0, and re-quantizing the fp32 dequantized chunk gives the
+    # same bytes (a sign-dropping +0 addend would turn every -0 code into 0x0)
+    for seed in (3, 7):
+        x = synth.make_tensor((64, 4, 128), "bf16", seed=seed).f64
+        q = nvfp4.quantize_kv_chunk(x)
+        codes = nvfp4.unpack_codes(q["codes"])
+        assert (codes == 8).any()
+        d32 = nvfp4.dequantize_kv_chunk_rn32(q, 64, 4, 128).reshape(256, 128)
+        assert np.all(np.signbit(d32[codes == 8])) and not np.any(np.signbit(d32[codes == 0]))
+        q2 = nvfp4.quantize_kv_chunk(d32.reshape(64, 4, 128))
+        assert np.array_equal(q2["codes"], q["codes"]) and np.array_equal(q2["scales"], q["scales"])
+
+
 def test_zero_and_underflow_conventions():
     z = np.zeros((3, 32))
     c, s, g = nvfp4.quantize(z)
