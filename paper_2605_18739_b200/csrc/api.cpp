@@ -83,7 +83,6 @@ struct kvq_cache {
   std::vector<LayerState> layers;
   int64_t shot_start = 0, shot_len = 0;
   bool two_pass_only = false;  // debug: force the amax + quantize two-pass path
-  unsigned long long quant_epoch = 0;  // single-pass quantizer launches since the arena was zeroed
 };
 
 namespace {
@@ -127,7 +126,7 @@ DevStatus* status_ptr(const kvq_cache* c) { return reinterpret_cast<DevStatus*>(
 kvq_status reset_device(kvq_cache* c, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(c->arena, 0, c->L.total, st);
   if (e != cudaSuccess) return KVQ_ECUDA;
-  c->quant_epoch = 0;  // the grid-barrier counters were zeroed with the arena
+  // the grid-barrier slots and the device launch epoch were zeroed with the arena
   DevStatus init{0, 0, ~0ull};
   // status word: code 0, first_bad = max (a small H2D copy from a static host value)
   static DevStatus s_init = init;
@@ -238,7 +237,6 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   p.ext_amax = ext_amax;
   p.status = status_ptr(c);
   p.trace = kvq_trace_ptr();
-  p.epoch = c->quant_epoch;
   p.mode = quant_mode(c);
   p.mean_out = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
   p.partials_w = partials;
@@ -246,7 +244,6 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   cudaError_t e = c->two_pass_only ? cudaErrorNotSupported
                                    : launch_quantize_fused(p, reinterpret_cast<unsigned long long*>(c->arena + c->L.off_counters),
                                                            partials, sm_count(), st);
-  if (e == cudaSuccess && !ext_amax) c->quant_epoch++;  // the launch arrives G times on each counter
   if (e == cudaErrorNotSupported) {
     (void)cudaGetLastError();
     if (c->cfg.k_smoothing) {  // K row means (+ K_bar partials), then V's partials

@@ -8,7 +8,7 @@ namespace kvq {
 constexpr int kTileKeys = 128;     // keys per attention tile; slots are padded to a multiple
 constexpr int kNumPartials = 592;  // amax partials per tensor (4 x 148 SMs)
 constexpr int kMaxFusedCtas = 192;   // single-pass quantizer grid limit
-constexpr int kSlotU64 = 16;        // one 128-byte line per barrier slot: [K, V, pad...] u64
+constexpr int kSlotU64 = 16;        // one 128-byte line per barrier slot: K sector [0,4), V sector [4,8) u64
 constexpr int kMaxSegs = 48;       // key segments per attention call
 
 enum DType : int { DT_BF16 = 0, DT_FP32 = 1, DT_FP16 = 2 };
@@ -34,7 +34,6 @@ struct QuantParams {
   const uint32_t* partials;  // [2][kNumPartials] amax bit patterns, or null
   const float* ext_amax;     // [2] caller-supplied amax (Ulysses), or null
   unsigned long long* trace; // debug timeline (null in production)
-  unsigned long long epoch;  // single-pass launches so far on this cache (grid-barrier target)
   DevStatus* status;
   int mode;                  // kModeSearch | kModeSmoothK bits
   float* mean_out;           // K-smoothing: K row means, slot base for head 0, [H][head_stride_rows]

@@ -15,6 +15,8 @@
 //                       loads, block max, E4M3 scale, 16 E2M1 codes packed with the hardware
 //                       cvt.rn.satfinite.e2m1x2.f32, one 8-byte code store + one scale byte into
 //                       the head-major cache slot.  Pass-2 reads hit L2 (the chunk is 28.75 MB).
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -347,6 +349,18 @@ KVQ_DEV uint32_t smoothed_absmax_bits(const float (&v)[16], float m) {
   return fabsf(m) <= 3.402823466e38f ? bits : 0x7F800000u;
 }
 
+// bf16 -> fp32 (exact): the low element is w << 16, the high one w & 0xFFFF0000.  KVQ_UNPACK_PRMT of
+// the 8 shifts are PRMTs on the ALU pipe, the rest IMAD.U32 on the FMA pipe, to balance the two
+// pipes in the quantize loop (whose Markstein quotients are all FMA-pipe work).
+#ifndef KVQ_UNPACK_PRMT
+#define KVQ_UNPACK_PRMT 4
+#endif
+KVQ_DEV uint32_t bf16lo_prmt(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(r) : "r"(w));
+  return r;
+}
+
 template <int DT>
 KVQ_DEV void unpack_block16(const uint8_t* src, float (&v)[16]) {  // generic pointer (smem or global)
   if (DT == DT_BF16) {
@@ -354,7 +368,7 @@ KVQ_DEV void unpack_block16(const uint8_t* src, float (&v)[16]) {  // generic po
     const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k] = __uint_as_float(k < KVQ_UNPACK_PRMT ? bf16lo_prmt(w[k]) : w[k] << 16);
       v[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
     }
   } else {
@@ -408,176 +422,38 @@ __global__ void __launch_bounds__(256) smooth_amax_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------------------------
-// Single-pass quantize/append (the default when the chunk fits in aggregate shared memory): a
-// cooperative persistent grid, one CTA per SM.  Each CTA bulk-copies (TMA engine, one
-// cp.async.bulk per tensor) its contiguous slice of K and of V -- 194 KB per SM for the Wan chunk --
-// into shared memory, so HBM is read exactly once.  Per tensor: local amax from smem -> partial ->
-// grid barrier (tagged slots, no reset) -> g -> quantize the slice from smem.
-#ifndef KVQ_QUANT_THREADS
-#define KVQ_QUANT_THREADS 512
-#endif
-#ifndef KVQ_QUANT_NB
-#define KVQ_QUANT_NB 2
-#endif
-constexpr int kFusedThreads = KVQ_QUANT_THREADS;
-constexpr int kQNB = KVQ_QUANT_NB;  // blocks per thread per iteration
-#ifndef KVQ_QUANT_V_DELAY
-#define KVQ_QUANT_V_DELAY 0
-#endif
-constexpr bool kVDelay = KVQ_QUANT_V_DELAY != 0;
+// Two-launch path, second pass (chunks too large for the single-pass kernel's shared memory, or
+// forced for testing): after amax_kernel (or smooth_amax_kernel) has written per-CTA partials, every
+// CTA reduces them to the tensor amax (or takes the caller's, Ulysses) and quantizes its block range
+// from global memory (L2-resident after the first pass).  Per-block work as in quant_sp_kernel, with
+// the decode scale and its reciprocal computed per block; blocks outside Markstein's range are
+// queued and redone with IEEE divisions.
+constexpr int kQ2Threads = 512;
+constexpr int kQ2NB = 2;  // blocks per thread per iteration
 
-template <int DT>
-KVQ_DEV uint32_t smem_absmax(const uint8_t* s, int nbytes) {
-  uint32_t m = 0;
-  const uint32_t base = smem_u32(s);  // explicit ld.shared (LDS.128), four vectors in flight
-  int i = threadIdx.x * 16;
-  if (DT == DT_BF16) {  // accumulate packed |bf16| maxima (0.75 instr/element), convert once
-    uint32_t m2 = 0;
-    for (; i < nbytes; i += kFusedThreads * 16) {
-      const uint4 a = ld_shared_v4(base + i);
-      m2 = max_u16x2(m2, a.x & 0x7FFF7FFFu, a.y & 0x7FFF7FFFu);
-      m2 = max_u16x2(m2, a.z & 0x7FFF7FFFu, a.w & 0x7FFF7FFFu);
-    }
-    return max((m2 & 0xFFFFu) << 16, m2 & 0xFFFF0000u);
-  }
-  for (; i + 3 * kFusedThreads * 16 < nbytes; i += 4 * kFusedThreads * 16) {
-    const uint4 a = ld_shared_v4(base + i), b = ld_shared_v4(base + i + kFusedThreads * 16);
-    const uint4 c = ld_shared_v4(base + i + 2 * kFusedThreads * 16), d = ld_shared_v4(base + i + 3 * kFusedThreads * 16);
-    m = max(m, max(max(vec_absmax_bits<DT>(a), vec_absmax_bits<DT>(b)), max(vec_absmax_bits<DT>(c), vec_absmax_bits<DT>(d))));
-  }
-  for (; i < nbytes; i += kFusedThreads * 16) m = max(m, vec_absmax_bits<DT>(ld_shared_v4(base + i)));
-  return m;
-}
-
-// K-smoothing in the single-pass kernel: row means of the smem K slice (stored to smem and to the
-// cache's mean slot) and the slice max of |K_bar|.  Block i of the slice belongs to local row
-// i / kNB; the slice starts on a row boundary, so the kNB blocks of a row sit in kNB consecutive
-// lanes of one warp.
-template <int DT, int D>
-KVQ_DEV uint32_t smem_smooth_absmax(const QuantParams& p, const uint8_t* s, int nu, int64_t u0, float* s_mean) {
-  constexpr int kNB = D / 16;
-  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
-  const int tid = threadIdx.x;
-  uint32_t m = 0;
-  for (int base = tid & ~31; base < nu; base += kFusedThreads) {
-    const int i = base + (tid & 31);
-    const bool valid = i < nu;
-    float v[16];
-    if (valid) {
-      unpack_block16<DT>(s + (size_t)i * kUB, v);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
-    }
-    const float mean = row_mean<kNB>(v);
-    if (valid) {
-      m = max(m, smoothed_absmax_bits(v, mean));
-      if (i % kNB == 0) {
-        s_mean[i / kNB] = mean;
-        const int64_t row = (u0 + i) / kNB;
-        const int64_t t_tok = row / p.H, h = row - t_tok * p.H;
-        p.mean_out[h * p.head_stride_rows + t_tok] = mean;
-      }
-    }
-  }
-  return m;
-}
-
-// debug timeline (globaltimer ns) of CTA 0 (slots 0-7) and the last CTA (8-15) when p.trace is set
-#define QTRACE(ev)                                                                       \
-  do {                                                                                   \
-    if (p.trace != nullptr && tid == 0 && c < 256) {                                     \
-      unsigned long long t_;                                                             \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
-      p.trace[c * 8 + (ev)] = t_;                                                        \
-    }                                                                                    \
-  } while (0)
-
-// STAGED = true: the single-pass cooperative kernel described above.  STAGED = false: the second
-// pass of the two-launch path -- same per-block work, data read from global memory (L2-resident
-// after the amax pass), tensor amax reduced from the amax kernels' partials, ordinary launch.
-// MODE: kModeSearch (Four-Over-Six for K and V), kModeSmoothK (K-smoothing of K).
-template <int DT, int D, bool STAGED, int MODE>
-__global__ void __launch_bounds__(kFusedThreads, 1)
-    quant_fused_kernel(const __grid_constant__ QuantParams p, unsigned long long* slots, int upc) {
+template <int DT, int D, int MODE>
+__global__ void __launch_bounds__(kQ2Threads, 1) quant2_kernel(const __grid_constant__ QuantParams p, int upc) {
   constexpr bool SEARCH = (MODE & kModeSearch) != 0;
   constexpr bool SMOOTH = (MODE & kModeSmoothK) != 0;
-  const unsigned long long epoch = p.epoch;
   constexpr int kNB = D / 16;
   constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);  // bytes per 16-element block
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ uint64_t bar[2];
-  __shared__ uint32_t red2[2][kFusedThreads / 32];
   __shared__ uint32_t s_am[2];
   __shared__ int s_nq;
-  const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  const int c = blockIdx.x, tid = threadIdx.x;
   const int64_t NU = (int64_t)p.rows * kNB;
   const int64_t u0 = (int64_t)c * upc;
   const int64_t left = NU - u0;
   const int nu = left <= 0 ? 0 : (left < upc ? (int)left : upc);
-  const uint32_t slice = (uint32_t)upc * kUB;  // the V slice follows the K slice in smem
-  // flagged block indices [upc], then (single pass, smoothing) the K row means [upc / kNB]
-  uint32_t* queue = reinterpret_cast<uint32_t*>(STAGED ? sm + 2 * (size_t)slice : sm);
-  float* s_mean = reinterpret_cast<float*>(queue + upc);
+  uint32_t* queue = reinterpret_cast<uint32_t*>(sm);  // flagged block indices [upc]
   if (tid < 2) s_am[tid] = 0;
-  if (tid == 0) {
-    s_nq = 0;
-    mbar_init(bar + 0, 1);
-    mbar_init(bar + 1, 1);
-    fence_mbar_init();
-  }
+  if (tid == 0) s_nq = 0;
   __syncthreads();
-  // K is requested first; V (KVQ_QUANT_V_DELAY) only once this CTA's K slice has landed.
-  auto issue = [&](int t) {
-    mbar_arrive_expect_tx(bar + t, (uint32_t)nu * kUB);
-    bulk_g2s(sm + t * slice, (const uint8_t*)p.x[t] + u0 * kUB, (uint32_t)nu * kUB, bar + t);
-  };
-  if (STAGED && tid == 0 && nu > 0) {
-    issue(0);
-    if (!kVDelay) issue(1);
-  }
-  QTRACE(0);
-  // ---- global amax of K, then of V.  Barrier without fences or read-modify-write atomics: once
-  // its slice of tensor t has landed, CTA c publishes (epoch tag << 32 | its slice max) as one
-  // 64-bit store into its own 128-byte line (tag and value become visible together; one line per
-  // publisher keeps the pollers off a single L2 hot spot); then G threads of every CTA each poll one
-  // publisher's slot until its tag is this launch's epoch (epoch = earlier single-pass launches on
-  // this cache, host-tracked), and the CTA max-reduces.  Both tensors are published before K's
-  // slots are polled (quantizing K while V lands was measured slower: the code stores and the
-  // polling then compete with V's HBM reads); V's slots are loaded ahead, during K's quantization.
-  const uint32_t tag = (uint32_t)(epoch + 1);
-  if (STAGED && p.ext_amax == nullptr) {  // both slice maxima -> this CTA's slots
-    for (int t = 0; t < 2; ++t) {
-      if (nu > 0) mbar_wait(bar + t, 0);
-      if (t == 0 && kVDelay && tid == 0 && nu > 0) issue(1);
-      QTRACE(t == 0 ? 1 : 5);
-      const uint32_t lm = warp_max_u32(SMOOTH && t == 0 ? smem_smooth_absmax<DT, D>(p, sm, nu, u0, s_mean)
-                                                        : smem_absmax<DT>(sm + t * slice, nu * kUB));
-      if ((tid & 31) == 0) red2[t][tid >> 5] = lm;
-      __syncthreads();
-      if (tid == 0) {
-        uint32_t mm = 0;
-        for (int w = 0; w < kFusedThreads / 32; ++w) mm = max(mm, red2[t][w]);
-        const unsigned long long val = ((unsigned long long)tag << 32) | mm;
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slots + (size_t)c * kSlotU64 + t), "l"(val) : "memory");
-      }
-    }
-  } else if (p.ext_amax) {
-    // caller-supplied amax (Ulysses); with smoothing the caller's K amax is of K_bar, and the row
-    // means are computed here
-    if (STAGED && nu > 0) {
-      mbar_wait(bar + 0, 0);
-      if (kVDelay && tid == 0) issue(1);
-    }
-    if (SMOOTH) {
-      if (STAGED) (void)smem_smooth_absmax<DT, D>(p, sm, nu, u0, s_mean);
-    }
-    if (STAGED && nu > 0) mbar_wait(bar + 1, 0);
+  if (p.ext_amax) {  // caller-supplied amax (Ulysses); with smoothing, of K_bar
     if (tid < 2) s_am[tid] = __float_as_uint(p.ext_amax[tid]) & 0x7FFFFFFFu;
-    __syncthreads();
-  } else {  // two-pass: reduce the amax kernels' per-CTA partials
+  } else {  // reduce the amax kernels' per-CTA partials
     uint32_t mk = 0, mv = 0;
-    for (int k = tid; k < kNumPartials; k += kFusedThreads) {
+    for (int k = tid; k < kNumPartials; k += kQ2Threads) {
       mk = max(mk, p.partials[k]);
       mv = max(mv, p.partials[kNumPartials + k]);
     }
@@ -587,35 +463,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       atomicMax(&s_am[0], mk);
       atomicMax(&s_am[1], mv);
     }
-    __syncthreads();
   }
-  unsigned long long pre = 0;  // V slot loaded ahead (tid < G), checked after K is quantized
+  __syncthreads();
   for (int t = 0; t < 2; ++t) {
     const bool smooth_t = SMOOTH && t == 0;
-    if (STAGED && p.ext_amax == nullptr) {  // wait for every CTA's slot of tensor t
-      uint32_t m = 0;
-      for (int k = tid; k < G; k += kFusedThreads) {
-        unsigned long long a = k == tid ? pre : 0ull;
-        while ((uint32_t)(a >> 32) != tag) {
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(slots + (size_t)k * kSlotU64 + t) : "memory");
-          if ((uint32_t)(a >> 32) != tag) __nanosleep(32);
-        }
-        m = max(m, (uint32_t)a);
-      }
-      if (t == 0 && tid < G)
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(pre) : "l"(slots + (size_t)tid * kSlotU64 + 1) : "memory");
-      if ((tid & ~31) < G) {  // warps that polled (whole warps: the shuffle needs all lanes)
-        m = warp_max_u32(m);
-        if ((tid & 31) == 0) atomicMax(&s_am[t], m);
-      }
-      __syncthreads();
-      QTRACE(t == 0 ? 6 : 2);
-    }
-    const uint8_t* s = STAGED ? sm + t * slice : (const uint8_t*)p.x[t] + u0 * kUB;
+    const uint8_t* s = (const uint8_t*)p.x[t] + u0 * kUB;
     const uint32_t abits = s_am[t];
     if (abits >= 0x7F800000u) {  // non-finite tensor: leave the chunk undefined, report
       if (tid == 0 && c == 0) atomicCAS(&p.status->code, 0, -6);
-      for (int i = tid; i < nu * 16; i += kFusedThreads) {  // first offending element of this slice
+      for (int i = tid; i < nu * 16; i += kQ2Threads) {  // first offending element of this range
         const uint32_t bits = DT == DT_BF16 ? ((uint32_t)reinterpret_cast<const uint16_t*>(s)[i] & 0x7FFFu) << 16
                                             : reinterpret_cast<const uint32_t*>(s)[i] & 0x7FFFFFFFu;
         if (bits >= 0x7F800000u) atomicMin(&p.status->first_bad, (unsigned long long)(t * NU * 16 + u0 * 16 + i));
@@ -625,31 +481,30 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     const float amax = __uint_as_float(abits);
     const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
     const float rg = __frcp_rn(g);
-    const uint32_t all_exact = g >= 0x1p-60f && g <= 0x1p60f ? 0u : (1u << kQNB) - 1;  // Markstein range
+    const uint32_t all_exact = g >= 0x1p-60f && g <= 0x1p60f ? 0u : (1u << kQ2NB) - 1;  // Markstein range
     const float invH = 1.0f / (float)p.H;
     if (c == 0 && tid == 0) p.g_out[t] = g;
     uint8_t* codes = p.codes[t];
     uint8_t* scales = p.scales[t];
-    // two blocks per thread per iteration (independent streams for latency hiding)
-    for (int i = tid; i < nu; i += kQNB * kFusedThreads) {
-      int ib[kQNB];
-      int64_t orow[kQNB];
+    for (int i = tid; i < nu; i += kQ2NB * kQ2Threads) {
+      int ib[kQ2NB];
+      int64_t orow[kQ2NB];
 #pragma unroll
-      for (int b = 0; b < kQNB; ++b) ib[b] = i + b * kFusedThreads < nu ? i + b * kFusedThreads : i;
-      float v[kQNB][16];
+      for (int b = 0; b < kQ2NB; ++b) ib[b] = i + b * kQ2Threads < nu ? i + b * kQ2Threads : i;
+      float v[kQ2NB][16];
 #pragma unroll
-      for (int b = 0; b < kQNB; ++b) {
+      for (int b = 0; b < kQ2NB; ++b) {
         const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
         const uint32_t row = u / kNB;
         const uint32_t t_tok = div_small(row, (uint32_t)p.H, invH);
         orow[b] = (int64_t)(row - t_tok * (uint32_t)p.H) * p.head_stride_rows + t_tok;
         unpack_block16<DT>(s + (size_t)ib[b] * kUB, v[b]);
-        if (smooth_t) subtract_mean(v[b], STAGED ? s_mean[ib[b] / kNB] : p.mean_out[orow[b]]);
+        if (smooth_t) subtract_mean(v[b], p.mean_out[orow[b]]);
       }
-      uint32_t sb[kQNB], w0[kQNB], w1[kQNB];
-      const uint32_t flags = quantize_blocks_fast<kQNB, SEARCH>(v, g, rg, sb, w0, w1) | all_exact;
+      uint32_t sb[kQ2NB], w0[kQ2NB], w1[kQ2NB];
+      const uint32_t flags = quantize_blocks_fast<kQ2NB, SEARCH>(v, g, rg, sb, w0, w1) | all_exact;
 #pragma unroll
-      for (int b = 0; b < kQNB; ++b) {
+      for (int b = 0; b < kQ2NB; ++b) {
         if (b > 0 && ib[b] == ib[0]) break;
         if (flags & (1u << b)) queue[atomicAdd(&s_nq, 1)] = (uint32_t)ib[b];  // exact recompute below
         const int j = (int)(((uint32_t)u0 + (uint32_t)ib[b]) % kNB);
@@ -658,10 +513,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
     }
     __syncthreads();
-    if (t == 0) QTRACE(4);
     // deferred exact path for flagged blocks (out-of-range scales only; one thread per block)
     const int nq = s_nq;
-    for (int e = tid; e < nq; e += kFusedThreads) {
+    for (int e = tid; e < nq; e += kQ2Threads) {
       const int ibk = (int)queue[e];
       const uint32_t u = (uint32_t)u0 + (uint32_t)ibk;
       const uint32_t row = u / kNB;
@@ -671,7 +525,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int64_t orw = (int64_t)h * p.head_stride_rows + t_tok;
       float v[16];
       unpack_block16<DT>(s + (size_t)ibk * kUB, v);
-      if (smooth_t) subtract_mean(v, STAGED ? s_mean[ibk / kNB] : p.mean_out[orw]);
+      if (smooth_t) subtract_mean(v, p.mean_out[orw]);
       uint32_t sbe, a, bb;
       quantize_block16_exact<SEARCH>(v, g, sbe, a, bb);
       *reinterpret_cast<uint2*>(codes + orw * (D / 2) + j * 8) = make_uint2(a, bb);
@@ -679,10 +533,390 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     __syncthreads();
     if (tid == 0) s_nq = 0;
-    QTRACE(3 + 4 * t);
   }
 }
-#undef QTRACE
+
+// ---------------------------------------------------------------------------------------------
+// Single-pass quantize/append, pipelined (quant_sp_kernel; the default when the chunk fits in
+// aggregate shared memory).  A cooperative grid of one CTA per SM; CTA c owns the contiguous
+// block range [u0, u0 + nu) of both K and V (rows t-major, 16-element blocks) and stages it in
+// shared memory with TMA bulk copies, so HBM is read exactly once.  The slice of each tensor is cut
+// into kSpPieces pieces with their own mbarriers: all K pieces are requested at once, V piece k only
+// when K piece k has landed, so the memory system serves K first and V streams in while K is being
+// quantized.  Per tensor:
+//   A. as pieces land: per-block max |x| (integer max on the bit patterns -- NaN-safe) -> smem, and
+//      the slice max -> the CTA's barrier slot (epoch tag << 32 | max bits, one 64-bit store);
+//   B. grid barrier: G threads of every CTA poll one slot each until its tag is this launch's; the
+//      tensor amax gives g = RN32(amax / 2688) (reading Z1);
+//   C. per E4M3 scale byte s a table of (d_b = RN32(dec(s) g), -RN32(1/d_b)) (128 entries, one
+//      correctly rounded reciprocal each), then every block: t = RN32(bmax/g), u = RN32(t/6),
+//      s = E4M3(u), codes E2M1(RN32(x/d_b)) by Markstein's correction with the
+//      tabulated reciprocal -- bit-identical to definition R1 (reading Z4) -- packed and stored
+//      head-major into the cache slot.
+// Order: A(K) B(K) C(K) A(V) B(V) C(V).  The launch epoch lives on the device (the word after the
+// CTA slots): every CTA reads it at start, CTA 0 advances it once the V barrier proves that all
+// CTAs have read it -- so a captured graph can replay the same launch any number of times.
+#ifndef KVQ_SP_THREADS
+#define KVQ_SP_THREADS 512
+#endif
+#ifndef KVQ_SP_NB
+#define KVQ_SP_NB 2
+#endif
+constexpr int kSpThreads = KVQ_SP_THREADS;
+constexpr int kSpNB = KVQ_SP_NB;  // blocks per thread per iteration of the quantize loop
+#ifndef KVQ_SP_PIECES
+#define KVQ_SP_PIECES 4
+#endif
+#ifndef KVQ_SP_EXP
+#define KVQ_SP_EXP 0      // timing experiments only (wrong results): 1 no stores, 2 no codes, 3 no smem loads, 4 skeleton, 5 no loop
+#endif
+#ifndef KVQ_SP_SLEEP
+#define KVQ_SP_SLEEP 32   // barrier poll back-off (ns)
+#endif
+constexpr int kSpPieces = KVQ_SP_PIECES;
+constexpr int kEpochLine = kMaxFusedCtas - 1;  // barrier line holding the device launch epoch
+
+// 8 codes per word from a 16-element block given d_b and ny = -RN32(1/d_b) (see codes_markstein)
+KVQ_DEV void codes_markstein_ny(const float (&v)[16], float db, float ny, uint32_t& w0, uint32_t& w1) {
+  const uint64_t ny2 = f32x2_pack(ny, ny), db2 = f32x2_pack(db, db);
+  float q[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t x2 = f32x2_pack(v[2 * k], v[2 * k + 1]);
+    const uint64_t q0 = fmul2(x2, ny2);
+    const uint64_t e = ffma2(q0, db2, x2);
+    const uint64_t q1 = ffma2(e, ny2, q0);
+    f32x2_unpack(q1, q[2 * k], q[2 * k + 1]);
+  }
+  w0 = e2m1x8(q) ^ 0x88888888u;
+  w1 = e2m1x8(q + 8) ^ 0x88888888u;
+}
+
+// max |x| of one staged 16-element block as fp32 bits (integer max: +inf/NaN stay >= 0x7F800000)
+template <int DT>
+KVQ_DEV uint32_t block_absmax_bits(uint32_t addr) {
+  if (DT == DT_BF16) {
+    const uint4 a = ld_shared_v4(addr), b = ld_shared_v4(addr + 16);
+    uint32_t m2 = max_u16x2(a.x & 0x7FFF7FFFu, a.y & 0x7FFF7FFFu, a.z & 0x7FFF7FFFu);
+    m2 = max_u16x2(m2, a.w & 0x7FFF7FFFu, b.x & 0x7FFF7FFFu);
+    m2 = max_u16x2(m2, b.y & 0x7FFF7FFFu, b.z & 0x7FFF7FFFu);
+    m2 = max_u16x2(m2, b.w & 0x7FFF7FFFu, 0u);
+    return max((m2 & 0xFFFFu) << 16, m2 & 0xFFFF0000u);
+  } else {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m = max(m, vec_absmax_bits<DT>(ld_shared_v4(addr + 16 * k)));
+    return m;
+  }
+}
+
+// (t, h) of a cache row, advanced by a fixed number of rows per step without division
+struct RowCursor {
+  uint32_t t, h;
+  KVQ_DEV void advance(uint32_t dq, uint32_t dr, uint32_t H) {
+    t += dq;
+    h += dr;
+    if (h >= H) { h -= H; ++t; }
+  }
+};
+
+#define SPTRACE(ev)                                                                      \
+  do {                                                                                   \
+    if (p.trace != nullptr && tid == 0 && c < 256) {                                     \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      p.trace[c * 16 + (ev)] = t_;                                                       \
+    }                                                                                    \
+  } while (0)
+
+template <int DT, int D, int MODE>
+__global__ void __launch_bounds__(kSpThreads, 1)
+    quant_sp_kernel(const __grid_constant__ QuantParams p, unsigned long long* slots, int upc) {
+  constexpr bool SEARCH = (MODE & kModeSearch) != 0;
+  constexpr bool SMOOTH = (MODE & kModeSmoothK) != 0;
+  constexpr int kNB = D / 16;
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);  // bytes per staged 16-element block
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar[2][kSpPieces];
+  __shared__ uint32_t red[2][kSpThreads / 32];
+  __shared__ uint32_t s_am[2];
+  __shared__ float2 tab[2][128];
+  __shared__ float s_g[2], s_rg[2];
+  __shared__ unsigned long long s_epoch;
+  const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  const int64_t NU = (int64_t)p.rows * kNB;
+  const int64_t u0 = (int64_t)c * upc;
+  const int nu = NU - u0 <= 0 ? 0 : (NU - u0 < upc ? (int)(NU - u0) : upc);
+  const uint32_t slice = (uint32_t)upc * kUB;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(sm + 2 * (size_t)slice);  // [2][upc] block max bits
+  float* s_mean = reinterpret_cast<float*>(bm + 2 * upc);             // SMOOTH: [upc / kNB] K row means
+  int ppc = (nu + kSpPieces - 1) / kSpPieces;
+  ppc = (ppc + kNB - 1) / kNB * kNB;  // pieces start on row boundaries
+  const bool ext = p.ext_amax != nullptr;
+  unsigned long long* epoch_word = slots + (size_t)kEpochLine * kSlotU64;
+  auto piece_lo = [&](int k) { return min(k * ppc, nu); };
+  auto issue = [&](int t, int k) {
+    const int a = piece_lo(k), b = piece_lo(k + 1);
+    if (b > a) {
+      mbar_arrive_expect_tx(&bar[t][k], (uint32_t)(b - a) * kUB);
+      bulk_g2s(sm + t * slice + (size_t)a * kUB, (const uint8_t*)p.x[t] + (u0 + a) * kUB, (uint32_t)(b - a) * kUB,
+               &bar[t][k]);
+    }
+  };
+  if (tid == 0) {
+    for (int k = 0; k < kSpPieces; ++k) {
+      mbar_init(&bar[0][k], 1);
+      mbar_init(&bar[1][k], 1);
+    }
+    fence_mbar_init();
+    unsigned long long e = 0;  // requested ahead of the chunk's TMA stream (not queued behind it)
+    if (!ext) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(e) : "l"(epoch_word) : "memory");
+    for (int k = 0; k < kSpPieces; ++k) issue(0, k);
+    s_epoch = e;
+  }
+  SPTRACE(0);
+  __syncthreads();
+  const uint32_t tag = (uint32_t)(s_epoch + 1);
+  const uint32_t sbase = smem_u32(sm);
+
+  // ---- A(t): per-block max |x| as pieces land -> smem; slice max -> this CTA's slot
+  auto phase_a = [&](int t) {
+    const uint32_t xs = sbase + (uint32_t)t * slice;
+    uint32_t* bmt = bm + t * upc;
+    uint32_t m = 0;
+#pragma unroll 1
+    for (int k = 0; k < kSpPieces; ++k) {
+      const int a = piece_lo(k), b = piece_lo(k + 1);
+      if (b <= a) break;
+      mbar_wait(&bar[t][k], 0);
+      if (t == 0 && tid == 0) issue(1, k);  // V piece k is requested once K piece k has landed
+      if (SMOOTH && t == 0) {
+        // row means (fixed fp32 tree order, reading Z20) need the kNB blocks of a row in one warp
+        for (int base = a + (tid & ~31); base < b; base += kSpThreads) {
+          const int i = base + (tid & 31);
+          const bool valid = i < b;
+          float v[16];
+          if (valid) {
+            unpack_block16<DT>(sm + (size_t)i * kUB, v);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0.0f;
+          }
+          const float mean = row_mean<kNB>(v);
+          if (valid) {
+            const uint32_t mb = smoothed_absmax_bits(v, mean);
+            bmt[i] = mb;
+            m = max(m, mb);
+            if (i % kNB == 0) {
+              s_mean[i / kNB] = mean;
+              const int64_t row = (u0 + i) / kNB;
+              const int64_t t_tok = row / p.H, h = row - t_tok * p.H;
+              p.mean_out[h * p.head_stride_rows + t_tok] = mean;
+            }
+          }
+        }
+      } else {
+        for (int i = a + tid; i < b; i += kSpThreads) {
+          const uint32_t mb = block_absmax_bits<DT>(xs + (uint32_t)i * kUB);
+          bmt[i] = mb;
+          m = max(m, mb);
+        }
+      }
+    }
+    SPTRACE(t == 0 ? 1 : 5);
+    m = warp_max_u32(m);
+    if ((tid & 31) == 0) red[t][tid >> 5] = m;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t mm = 0;
+      for (int w = 0; w < kSpThreads / 32; ++w) mm = max(mm, red[t][w]);
+      if (!ext) {
+        // the whole 32-byte sector is written (tag|max four times): a sector that is only partly
+        // written holds no valid copy in L2, and a poll of it would wait for a DRAM fill
+        const unsigned long long val = ((unsigned long long)tag << 32) | mm;
+        unsigned long long* sec = slots + (size_t)c * kSlotU64 + 4 * t;
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %1};" ::"l"(sec), "l"(val) : "memory");
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %1};" ::"l"(sec + 2), "l"(val) : "memory");
+      }
+      s_am[t] = ext ? (__float_as_uint(p.ext_amax[t]) & 0x7FFFFFFFu) : 0u;
+    }
+    __syncthreads();
+  };
+  // ---- B(t): grid barrier on tensor t (G threads poll one CTA slot each)
+  auto phase_b = [&](int t) {
+    if (ext) return;
+    uint32_t mg = 0;
+    if (tid < G) {
+      unsigned long long a;
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(slots + (size_t)tid * kSlotU64 + 4 * t) : "memory");
+        if ((uint32_t)(a >> 32) == tag) break;
+        __nanosleep(KVQ_SP_SLEEP);
+      }
+      mg = (uint32_t)a;
+    }
+    if ((tid & ~31) < G) {
+      mg = warp_max_u32(mg);
+      if ((tid & 31) == 0) atomicMax(&s_am[t], mg);
+    }
+    __syncthreads();
+    if (t == 1 && c == 0 && tid == 0)  // every CTA has read the epoch (it published V): advance it
+      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %1};\n st.relaxed.gpu.global.v2.u64 [%2], {%1, %1};"
+                   ::"l"(epoch_word), "l"(s_epoch + 1), "l"(epoch_word + 2) : "memory");
+    SPTRACE(t == 0 ? 6 : 2);
+  };
+  // ---- T(t0..t1): g = RN32(amax / 2688) and the decode-scale table per tensor
+  auto phase_t = [&](int t0, int nt) {
+    if (tid < 128 * nt) {
+      const int t = t0 + (tid >> 7), e = tid & 127;
+      const uint32_t abits = s_am[t];
+      const float amax = __uint_as_float(abits);
+      const float g = abits >= 0x7F800000u ? 1.0f : (amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f));
+      const float db = __fmul_rn(e4m3_to_f32((uint32_t)e), g);
+      tab[t][e] = make_float2(db, e == 0 ? -1.0f : -__frcp_rn(db));
+      if (e == 0) {
+        s_g[t] = g;
+        s_rg[t] = __frcp_rn(g);
+        if (c == 0 && abits < 0x7F800000u) p.g_out[t] = g;
+      }
+    }
+    __syncthreads();
+    SPTRACE(8 + t0);
+  };
+  // ---- C (K, then V): quantize the staged slices (one code copy).
+  constexpr uint32_t kRowsStep = kSpThreads / kNB;  // rows advanced per kSpThreads blocks
+  const uint32_t H = (uint32_t)p.H, dq = kRowsStep / H, dr = kRowsStep % H;
+  const uint32_t hs = (uint32_t)p.head_stride_rows;
+  // output row orow = h * hs + t (head-major slot rows; < 2^26, so byte offsets fit in 32 bits)
+  const uint32_t ostep = dq + dr * hs, owrap = 1u - H * hs;  // (mod 2^32) when h wraps past H
+  const int j = tid % kNB;  // u0 is a multiple of kNB
+  uint32_t ch0, orow0;
+  {
+    const uint32_t row0 = (uint32_t)(u0 + tid) / kNB;
+    const uint32_t t0 = row0 / H;
+    ch0 = row0 - t0 * H;
+    orow0 = ch0 * hs + t0;
+  }
+  auto phase_c = [&](int t) {
+    const bool smooth_t = SMOOTH && t == 0;
+    const uint32_t* bmt = bm + t * upc;
+    const uint8_t* xs_t = sm + t * slice;
+    if (s_am[t] >= 0x7F800000u) {  // non-finite tensor: leave the chunk undefined, report the first index
+      if (tid == 0 && c == 0) atomicCAS(&p.status->code, 0, -6);
+      for (int i = tid; i < nu * 16; i += kSpThreads) {
+        const uint32_t bits = DT == DT_BF16 ? ((uint32_t)reinterpret_cast<const uint16_t*>(xs_t)[i] & 0x7FFFu) << 16
+                                            : reinterpret_cast<const uint32_t*>(xs_t)[i] & 0x7FFFFFFFu;
+        if (bits >= 0x7F800000u) atomicMin(&p.status->first_bad, (unsigned long long)(t * NU * 16 + u0 * 16 + i));
+      }
+      return;
+    }
+    const float g = s_g[t], rg = s_rg[t];
+    const float2* tb = tab[t];
+    uint8_t* codes = p.codes[t];
+    uint8_t* scales = p.scales[t];
+    uint32_t ch = ch0, orow = orow0;
+    // Markstein's conditions (no under/overflow) hold for every block when 2^-55 <= g <= 2^60
+    // (d_b >= 2^-9 g >= 2^-64); outside (amax < 2e-13 or > 3e21) every block takes the IEEE path
+    if (!(g >= 0x1p-55f && g <= 0x1p60f)) {
+#pragma unroll 1
+      for (int i = tid; i < nu; i += kSpThreads) {
+        const uint32_t row = (uint32_t)(u0 + i) / kNB, tt = row / H, hh = row - tt * H;
+        const uint32_t ob = hh * hs + tt;
+        float v[16];
+        unpack_block16<DT>(xs_t + (size_t)i * kUB, v);
+        if (smooth_t) subtract_mean(v, s_mean[i / kNB]);
+        uint32_t sb, a0, a1;
+        quantize_block16_exact<SEARCH>(v, g, sb, a0, a1);
+        *reinterpret_cast<uint2*>(codes + (ob * (uint32_t)(D / 2) + (uint32_t)j * 8u)) = make_uint2(a0, a1);
+        scales[ob * (uint32_t)kNB + (uint32_t)j] = (uint8_t)sb;
+      }
+      return;
+    }
+    int it_ = 0;
+    for (int i = tid; i < (KVQ_SP_EXP == 5 ? 0 : nu); i += kSpNB * kSpThreads, ++it_) {
+      if (it_ == 1) SPTRACE(10 + t);
+      if (it_ == 2) SPTRACE(12 + t);
+      float v[kSpNB][16];
+      uint32_t sb[kSpNB], w0[kSpNB], w1[kSpNB], ob[kSpNB];
+#pragma unroll
+      for (int b = 0; b < kSpNB; ++b) {
+        ob[b] = orow;
+        ch += dr;
+        orow += ostep;
+        if (ch >= H) {
+          ch -= H;
+          orow += owrap;
+        }
+        const int ib = min(i + b * kSpThreads, nu - 1);
+#if KVQ_SP_EXP == 4 || KVQ_SP_EXP == 6  // timing experiment: loop skeleton (cursor, block max load, stores (4))
+        w0[b] = bmt[ib];
+        w1[b] = w0[b] ^ 0x5555u;
+        sb[b] = w0[b] & 0x7F;
+        continue;
+#endif
+#if KVQ_SP_EXP == 7  // timing experiment: codes stores only (no scale-byte stores)
+        sb[b] = 0;
+#endif
+#if KVQ_SP_EXP == 3  // timing experiment: no smem loads
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[b][e] = __uint_as_float(0x3F800000u + (uint32_t)(ib * 16 + e));
+#else
+        unpack_block16<DT>(xs_t + (size_t)ib * kUB, v[b]);
+#endif
+        if (smooth_t) subtract_mean(v[b], s_mean[ib / kNB]);
+        const float bmax = __uint_as_float(bmt[ib]);
+        const float tq = div_markstein(bmax, g, rg);
+        uint32_t s = scale_byte(div_markstein(tq, 6.0f, 0.16666667163372040f), bmax);  // RN32(1/6)
+        const float2 e = tb[s];
+#if KVQ_SP_EXP == 2  // timing experiment: no element codes
+        w0[b] = __float_as_uint(v[b][0] * e.x + v[b][5]);
+        w1[b] = __float_as_uint(v[b][9] * e.y + v[b][15]);
+#else
+        codes_markstein_ny(v[b], e.x, e.y, w0[b], w1[b]);
+#endif
+        if (SEARCH) {  // Four-Over-Six: the 4-target scale wins when strictly better
+          const uint32_t s4 = scale_byte(__fmul_rn(tq, 0.25f), bmax);
+          if (s4 != s) {
+            const float2 e4 = tb[s4];
+            uint32_t a0, a1;
+            codes_markstein_ny(v[b], e4.x, e4.y, a0, a1);
+            if (block_sse(v[b], a0, a1, s4, g) < block_sse(v[b], w0[b], w1[b], s, g)) {
+              s = s4;
+              w0[b] = a0;
+              w1[b] = a1;
+            }
+          }
+        }
+        const bool z = s == 0;
+        w0[b] = z ? 0u : w0[b];
+        w1[b] = z ? 0u : w1[b];
+        sb[b] = s;
+      }
+#pragma unroll
+      for (int b = 0; b < kSpNB; ++b) {
+        if (i + b * kSpThreads < nu && ((KVQ_SP_EXP != 1 && KVQ_SP_EXP != 6) || w0[b] == 0x12345678u)) {
+          *reinterpret_cast<uint2*>(codes + (ob[b] * (uint32_t)(D / 2) + (uint32_t)j * 8u)) = make_uint2(w0[b], w1[b]);
+          if (KVQ_SP_EXP != 7) scales[ob[b] * (uint32_t)kNB + (uint32_t)j] = (uint8_t)sb[b];
+        }
+      }
+    }
+    SPTRACE(t == 0 ? 3 : 7);
+  };
+  // schedule: A(K) A(V), then (B T C) per tensor.  Both tensors are published before either barrier is
+  // polled (a barrier takes ~1-2 us to resolve while the chunk's TMA stream is in flight, so K's
+  // resolves as V lands), and V's barrier latency overlaps K's quantization.  One code copy per
+  // phase (loops, not unrolled): the instruction cache stays warm for the second tensor.
+#pragma unroll 1
+  for (int t = 0; t < 2; ++t) phase_a(t);
+#pragma unroll 1
+  for (int t = 0; t < 2; ++t) {
+    phase_b(t);
+    phase_t(t, 1);
+    phase_c(t);
+  }
+}
+
+#undef SPTRACE
 
 // Eq. 2: x^ = dec(c) dec(s) g.  dec(c) dec(s) is exact in fp32 (<= 7 significant
 // bits), so one FMA with g (and the K-smoothing row mean, else -0) rounds the exact value once.
@@ -849,18 +1083,21 @@ cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, i
   const int64_t NU = (int64_t)p.rows * (D / 16);
   int upc = (int)((NU + sms - 1) / sms);
   if (upc < 64) upc = 64;
-  upc = (upc + 7) & ~7;  // 128-byte aligned V slice
+  upc = (upc + 7) & ~7;  // 128-byte aligned V slice, slices on row boundaries
   const int G = (int)((NU + upc - 1) / upc);
-  // K, V slices + flag queue (+ K row means with smoothing)
-  const size_t smem = (size_t)2 * upc * kUB + (size_t)upc * sizeof(uint32_t) +
+  // K, V slices + per-block max bits (+ K row means with smoothing)
+  const size_t smem = (size_t)2 * upc * kUB + (size_t)2 * upc * sizeof(uint32_t) +
                       ((MODE & kModeSmoothK) ? (size_t)(upc / (D / 16)) * sizeof(float) : 0);
-  if (smem > 220 * 1024 || G > kNumPartials || G > kMaxFusedCtas) return cudaErrorNotSupported;
-  auto kern = quant_fused_kernel<DT, D, true, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = quant_sp_kernel<DT, D, MODE>;
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  if (smem + fa.sharedSizeBytes > 227 * 1024 || G >= kEpochLine) return cudaErrorNotSupported;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(kFusedThreads);
+  cfg.blockDim = dim3(kSpThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -868,7 +1105,8 @@ cudaError_t launch_fused_t(const QuantParams& p, unsigned long long* counters, i
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // counters -> the barrier slots: [G] lines of kSlotU64 u64, (tag << 32 | amax bits) for K and V
+  // counters -> the barrier slots: [G] lines of kSlotU64 u64 (tag << 32 | amax bits) for K and V,
+  // line kEpochLine = the device launch epoch
   return cudaLaunchKernelEx(&cfg, kern, p, counters, upc);
 }
 
@@ -882,10 +1120,10 @@ cudaError_t launch_quant2_t(const QuantParams& p, int sms, cudaStream_t st) {
   upc = (upc + 7) & ~7;  // slices start on row boundaries
   G = (NU + upc - 1) / upc;
   const size_t smem = (size_t)upc * sizeof(uint32_t);
-  auto kern = quant_fused_kernel<DT, D, false, MODE>;
+  auto kern = quant2_kernel<DT, D, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)G, kFusedThreads, smem, st>>>(p, nullptr, upc);
+  kern<<<(unsigned)G, kQ2Threads, smem, st>>>(p, upc);
   return cudaGetLastError();
 }
 

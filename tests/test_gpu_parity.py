@@ -127,6 +127,32 @@ def test_quantize_lattice_inputs_take_exact_path():
     assert np.array_equal(qk["codes"], ref["codes"]) and np.array_equal(qk["scales"], ref["scales"])
 
 
+def test_quantize_graph_replay_of_one_append_bitexact():
+    # one append captured in a CUDA graph and replayed with new inputs: the single-pass kernel's grid
+    # barrier must not pass on a previous replay's tags (the launch epoch lives on the device)
+    _gpu()
+    T, H, d = 1560, 12, 128
+    c = _cache(H, d, 1560, 1)
+    _, k0, v0 = synth.make_qkv(T, H, d, "bf16", 0, 0)
+    K, V = k0.torch(DEV), v0.torch(DEV)
+    c.append(0, 0, K, V)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        c.append(0, 0, K, V)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        c.append(0, 0, K, V)
+    for rep in range(1, 5):
+        _, k, v = synth.make_qkv(T, H, d, "bf16", 0, rep, variant="outlier" if rep % 2 else "iid")
+        K.copy_(k.torch(DEV))
+        V.copy_(v.torch(DEV))
+        g.replay()
+        torch.cuda.synchronize()
+        assert_chunk_bytes_equal(c.export(0, 0), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
+
+
 def test_quantize_edge_blocks_bitexact():
     # zero tensor (g = 1), zero blocks, underflow-promoted scales, -0.0, ragged T_c (not a multiple of 128)
     _gpu()
