@@ -680,12 +680,29 @@ __global__ void __launch_bounds__(kSpThreads, 1)
   const uint32_t sbase = smem_u32(sm);
 
   // ---- A(t): per-block max |x| as pieces land -> smem; slice max -> this CTA's slot
-  auto phase_a = [&](int t) {
+  // Threads [wt0, kSpThreads) do the work; with wt0 > 0 (V, single-pass barrier) the first warps
+  // meanwhile poll K's barrier slots, so K's barrier resolves while V lands.
+  auto phase_a = [&](int t, int wt0) {
     const uint32_t xs = sbase + (uint32_t)t * slice;
     uint32_t* bmt = bm + t * upc;
+    const int wtid = tid - wt0, nw = kSpThreads - wt0;
     uint32_t m = 0;
+    if (wtid < 0) {  // K barrier pollers (G threads poll one CTA slot each)
+      uint32_t mg = 0;
+      if (tid < G) {
+        unsigned long long a;
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(slots + (size_t)tid * kSlotU64) : "memory");
+          if ((uint32_t)(a >> 32) == tag) break;
+          __nanosleep(KVQ_SP_SLEEP);
+        }
+        mg = (uint32_t)a;
+      }
+      mg = warp_max_u32(mg);
+      if ((tid & 31) == 0) atomicMax(&s_am[0], mg);
+    }
 #pragma unroll 1
-    for (int k = 0; k < kSpPieces; ++k) {
+    for (int k = 0; k < kSpPieces && wtid >= 0; ++k) {
       const int a = piece_lo(k), b = piece_lo(k + 1);
       if (b <= a) break;
       mbar_wait(&bar[t][k], 0);
@@ -716,7 +733,7 @@ __global__ void __launch_bounds__(kSpThreads, 1)
           }
         }
       } else {
-        for (int i = a + tid; i < b; i += kSpThreads) {
+        for (int i = a + wtid; i < b; i += nw) {
           const uint32_t mb = block_absmax_bits<DT>(xs + (uint32_t)i * kUB);
           bmt[i] = mb;
           m = max(m, mb);
@@ -743,12 +760,13 @@ __global__ void __launch_bounds__(kSpThreads, 1)
     __syncthreads();
   };
   // ---- B(t): grid barrier on tensor t (G threads poll one CTA slot each)
+  unsigned long long vpre = 0;  // V slot loaded ahead (at the start of K's quantization)
   auto phase_b = [&](int t) {
     if (ext) return;
     uint32_t mg = 0;
     if (tid < G) {
-      unsigned long long a;
-      for (;;) {
+      unsigned long long a = t == 1 ? vpre : 0ull;
+      while ((uint32_t)(a >> 32) != tag) {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(slots + (size_t)tid * kSlotU64 + 4 * t) : "memory");
         if ((uint32_t)(a >> 32) == tag) break;
         __nanosleep(KVQ_SP_SLEEP);
@@ -810,6 +828,8 @@ __global__ void __launch_bounds__(kSpThreads, 1)
       }
       return;
     }
+    if (t == 0 && !ext && tid < G)  // V's slot, requested now and consumed after K's loop
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(vpre) : "l"(slots + (size_t)tid * kSlotU64 + 4) : "memory");
     const float g = s_g[t], rg = s_rg[t];
     const float2* tb = tab[t];
     uint8_t* codes = p.codes[t];
@@ -902,15 +922,17 @@ __global__ void __launch_bounds__(kSpThreads, 1)
     }
     SPTRACE(t == 0 ? 3 : 7);
   };
-  // schedule: A(K) A(V), then (B T C) per tensor.  Both tensors are published before either barrier is
-  // polled (a barrier takes ~1-2 us to resolve while the chunk's TMA stream is in flight, so K's
-  // resolves as V lands), and V's barrier latency overlaps K's quantization.  One code copy per
-  // phase (loops, not unrolled): the instruction cache stays warm for the second tensor.
-#pragma unroll 1
-  for (int t = 0; t < 2; ++t) phase_a(t);
+  // schedule: A(K), then A(V) on most warps while the first warps poll K's barrier (a barrier takes
+  // ~1-2 us to resolve while the chunk's TMA stream is in flight), then (T C) for K with V's slots
+  // requested at the start of K's loop, B(V), (T C) for V.  One code copy per phase (loops, not
+  // unrolled): the instruction cache stays warm for the second tensor.
+  phase_a(0, 0);
+  const int npoll = ext ? 0 : (G + 31) & ~31;  // warps that poll K's slots during A(V)
+  phase_a(1, npoll);
+  if (!ext) SPTRACE(6);
 #pragma unroll 1
   for (int t = 0; t < 2; ++t) {
-    phase_b(t);
+    if (t == 1) phase_b(1);
     phase_t(t, 1);
     phase_c(t);
   }

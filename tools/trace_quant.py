@@ -1,7 +1,7 @@
-"""Phase timeline (ns, globaltimer) of the single-pass quantize kernel over all CTAs (development aid).
-Events per CTA: 0 start, 1 K landed, 5 V landed, 6 K amax known (after polling every CTA's slot),
-8 K table, 10/12 K loop iterations 1/2 done, 3 K quantized, 2 V amax known, 9 V table, 11/13 V iterations,
-7 V quantized (steady state inside a graph of appends)."""
+"""Phase timeline (ns, globaltimer, median/max over CTAs) of the single-pass quantize kernel in steady
+state (development aid).  Events per CTA (thread 0): 0 start, 1 K landed + published, 5 K barrier
+seen (thread 0 is a K poller during A(V)), 6 V landed + published, 8 K table, 10/12 K loop
+iterations 1/2 done, 3 K quantized, 2 V barrier, 9 V table, 11/13 V iterations, 7 V quantized."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -38,7 +38,7 @@ t = tr.view(256, 16).cpu().numpy().astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 t = t - t0
-names = {0: "start", 1: "K landed", 5: "V landed", 6: "K barrier", 8: "K table", 10: "K it1", 12: "K it2", 3: "K quant",
-         2: "V barrier", 9: "V table", 11: "V it1", 13: "V it2", 7: "V quant"}
+names = {0: "start", 1: "K landed", 5: "K barrier seen", 6: "V landed+published", 8: "K table", 10: "K it1",
+         12: "K it2", 3: "K quant", 2: "V barrier", 9: "V table", 11: "V it1", 13: "V it2", 7: "V quant"}
 print(f"{len(t)} CTAs: " + "  ".join(f"{n}: {int(np.median(t[:, e]))}/{t[:, e].max()}" for e, n in names.items()
                                      if t[:, e].min() >= 0))
