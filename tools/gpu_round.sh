@@ -16,7 +16,7 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
      python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_bench_$TAG.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_ws -s 8 -c 1 \
      -o gpurun_out/attn_$TAG -f python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_attn_$TAG.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_fused -s 8 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:quant_sp -s 8 -c 1 \
      -o gpurun_out/quant_$TAG -f python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_quant_$TAG.log 2>&1
   ls gpurun_out | grep $TAG
 fi

@@ -43,7 +43,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size", "sm__cycles_elapsed.avg.per_second", "smsp__inst_executed.sum"]
 traffic = {}
-for rep, label in ((f"attn_{tag}", "attn_ws_kernel"), (f"quant_{tag}", "quant_fused_kernel")):
+for rep, label in ((f"attn_{tag}", "attn_ws_kernel"), (f"quant_{tag}", "quant_sp_kernel")):
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
