@@ -171,7 +171,7 @@ def run_gpu(args):
         q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, ch)
         chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
     dq = [tuple(x.to(dev) for x in c) for c in chunks]
-    uly = kvq.Ulysses(cache, H, D, T_C, rank, P) if P > 1 else None
+    uly = kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4") if P > 1 else None
 
     def step(c, out=None):
         q, k, v = dq[c]
@@ -303,6 +303,7 @@ def run_gpu(args):
            "config": {"workload": WORKLOAD, "heads": H, "head_dim": D, "T_c": T_C, "tokens_per_frame": TPF,
                       "frames_per_chunk": T_FRAMES, "sink_frames": SINK, "window_frames": WINDOW,
                       "n_keys": nk, "chunk_index": CHUNK, "parallelism": f"ulysses-heads{world}" if world > 1 else "1 GPU",
+                      "exchange": args.exchange if world > 1 else None,
                       "l2": "flushed (256 MiB write) before every timed step"},
            # per step: N=1 quantize/append (1) + attention (1) + split-KV combine (1);
            # N>1 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted)
@@ -422,6 +423,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4"],
+                    help="N>1: K/V payload of the all-to-all (nvfp4 = §8(f) f3, quantized on the sender)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

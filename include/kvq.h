@@ -209,6 +209,47 @@ kvq_status kvq_ulysses_unpack_qkv(const void* recv_buf, kvq_dtype dtype, int32_t
 kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t Ts, int32_t H,
                                 int32_t d, int32_t P, void* O_shard, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NVFP4 payload for the exchange (§8(f) f3; App. D: the pre-attention
+ * All-to-All "performed entirely in the low-precision space", ~3.6x less K/V volume).  The
+ * sender quantizes its sequence shard of K and V with the GLOBAL tensor scales, so what it ships
+ * is exactly the cache bytes of the 1-GPU run for those rows (readings Z2/Z18); Q travels in its
+ * input dtype (the paper's NVFP4 Q changes the attention numerics and is not built).  Sequence:
+ *   kvq_ulysses_shard_amax -> all-reduce(MAX) of the 2 floats over the group (NCCL) ->
+ *   kvq_ulysses_pack_nvfp4 -> all_to_all_single -> kv_append_ulysses_nvfp4 -> chunk_attention. */
+
+/* Device scratch for kvq_ulysses_shard_amax (partials, status, K-smoothing means). */
+size_t kvq_ulysses_shard_scratch_bytes(int32_t Ts, int32_t H);
+
+/* amax of this rank's shard: dev_amax_kv fp32[2] = max |K| (max |K - row mean| with
+ * k_smoothing, reading Z20) and max |V| over the shard [Ts, H, d]; non-finite values propagate
+ * (the receiving cache reports KVQ_ENONFINITE). */
+kvq_status kvq_ulysses_shard_amax(const void* K, const void* V, kvq_dtype dtype, int32_t Ts,
+                                  int32_t H, int32_t d, int32_t k_smoothing, float* dev_amax_kv,
+                                  void* dev_scratch, void* stream);
+
+/* Bytes of the segment for destination `dst` (= bytes received from every source when dst is
+ * this rank): per row (t, h_dst) Q d*esize(q_dtype), K and V codes d/2 + scales d/16 each (+ a
+ * fp32 K mean with k_smoothing), each part padded to 16 bytes. */
+size_t kvq_ulysses_nvfp4_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst,
+                               kvq_dtype q_dtype, int32_t k_smoothing);
+
+/* Quantize + pack this rank's shard (Q, K, V dev [Ts, H, d]) into the all-to-allv send buffer,
+ * destination segments in rank order.  dev_amax_kv: the GLOBAL amax (all-reduced) -> g =
+ * RN32(amax/2688); scale_mode / k_smoothing must match the receiving caches' config. */
+kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, kvq_dtype dtype,
+                                  int32_t Ts, int32_t H, int32_t d, int32_t P,
+                                  const float* dev_amax_kv, int32_t scale_mode,
+                                  int32_t k_smoothing, void* send_buf, void* stream);
+
+/* Receiving side: the P received segments (this rank's H_r = cache num_heads heads, Ts = T_c/P
+ * tokens each) become chunk `chunk_index` of `layer` under the append policy of
+ * kv_quantize_append (same slot / eviction rules, same error codes), g of the slot from
+ * dev_amax_kv, and Q_out dev [T_c, H_r, d] (q_dtype) receives the chunk's queries. */
+kvq_status kv_append_ulysses_nvfp4(kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                                   const void* recv_buf, int32_t P, const float* dev_amax_kv,
+                                   void* Q_out, kvq_dtype q_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -187,18 +187,16 @@ kvq_status resolve_segments(const kvq_cache* c, int layer, const kvq_mask* m, st
   return KVQ_OK;
 }
 
-kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K, const void* V, kvq_dtype dt,
-                       const float* ext_amax, void* stream) {
-  if (!c || !K || !V) return KVQ_EINVAL;
-  if (layer < 0 || layer >= c->cfg.num_layers || chunk < 0) return KVQ_EINVAL;
-  if (dt != KVQ_BF16 && dt != KVQ_FP32) return KVQ_EDTYPE;
+// Slot of (layer, chunk) under the append policy: chunk == newest re-writes its slot (a denoising
+// step); chunk == newest + 1 evicts what K_eff of this and later steps can no longer reach (the
+// global sink, the bound shot sink and the window ending at the new chunk) and
+// takes a free slot; anything else is KVQ_ENOCHUNK.  Nothing is committed until commit_slot.
+static kvq_status select_slot(kvq_cache* c, int32_t layer, int64_t chunk, int* slot_out) {
   LayerState& ls = c->layers[layer];
   int slot = -1;
   if (ls.newest >= 0 && chunk == ls.newest) {
-    slot = ls.slot_of.at(chunk);  // denoising re-write of the in-progress chunk
+    slot = ls.slot_of.at(chunk);
   } else if (ls.newest < 0 || chunk == ls.newest + 1) {
-    // evict chunks that K_eff of this and later steps can no longer reach: keep the global sink,
-    // the bound shot sink and the window ending at the new chunk
     auto keep = chunks_of(key_token_ranges(chunk, c->cfg.frames_per_chunk, 1, c->cfg.sink_frames,
                                            c->cfg.window_frames, c->shot_start, c->shot_len),
                           c->cfg.frames_per_chunk);
@@ -216,6 +214,25 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   } else {
     return KVQ_ENOCHUNK;
   }
+  *slot_out = slot;
+  return KVQ_OK;
+}
+
+static void commit_slot(kvq_cache* c, int32_t layer, int64_t chunk, int slot) {
+  LayerState& ls = c->layers[layer];
+  ls.slot_of[chunk] = slot;
+  ls.chunk_in[slot] = chunk;
+  ls.newest = chunk;
+}
+
+kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K, const void* V, kvq_dtype dt,
+                       const float* ext_amax, void* stream) {
+  if (!c || !K || !V) return KVQ_EINVAL;
+  if (layer < 0 || layer >= c->cfg.num_layers || chunk < 0) return KVQ_EINVAL;
+  if (dt != KVQ_BF16 && dt != KVQ_FP32) return KVQ_EDTYPE;
+  int slot = -1;
+  const kvq_status ss = select_slot(c, layer, chunk, &slot);
+  if (ss != KVQ_OK) return ss;
   const int H = c->cfg.num_heads, d = c->cfg.head_dim;
   const int64_t rows = c->L.T_c * H;
   cudaStream_t st = S(stream);
@@ -258,9 +275,7 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
     e = launch_quantize2(p, sm_count(), st);
   }
   if (e != cudaSuccess) return KVQ_ECUDA;
-  ls.slot_of[chunk] = slot;
-  ls.chunk_in[slot] = chunk;
-  ls.newest = chunk;
+  commit_slot(c, layer, chunk, slot);
   return KVQ_OK;
 }
 
@@ -579,6 +594,106 @@ kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t T
   if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
   return cuda_status(launch_ulysses_unpack_o(static_cast<const uint8_t*>(recv_buf), dtype == KVQ_BF16 ? DT_BF16 : DT_FP32,
                                              Ts, H, d, P, O_shard, S(stream)));
+}
+
+// ---- NVFP4 payload exchange (§8(f) f3)
+size_t kvq_ulysses_shard_scratch_bytes(int32_t Ts, int32_t H) {
+  return 2 * kNumPartials * sizeof(uint32_t) + 64 + (size_t)Ts * H * sizeof(float);
+}
+
+size_t kvq_ulysses_nvfp4_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst, kvq_dtype q_dtype,
+                               int32_t k_smoothing) {
+  int32_t h0, h1;
+  kvq_head_partition(H, P, dst, &h0, &h1);
+  return (size_t)nvfp4_seg_layout(Ts, h1 - h0, d, (int)esize(q_dtype), k_smoothing != 0).total;
+}
+
+kvq_status kvq_ulysses_shard_amax(const void* K, const void* V, kvq_dtype dtype, int32_t Ts, int32_t H, int32_t d,
+                                  int32_t k_smoothing, float* dev_amax_kv, void* dev_scratch, void* stream) {
+  if (!K || !V || !dev_amax_kv || !dev_scratch || Ts <= 0 || H <= 0) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (k_smoothing != 0 && k_smoothing != 1) return KVQ_EINVAL;
+  uint8_t* sc = static_cast<uint8_t*>(dev_scratch);
+  uint32_t* partials = reinterpret_cast<uint32_t*>(sc);
+  DevStatus* status = reinterpret_cast<DevStatus*>(sc + 2 * kNumPartials * sizeof(uint32_t));
+  QuantParams p{};
+  p.x[0] = K;
+  p.x[1] = V;
+  p.dtype = dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.rows = Ts * H;
+  p.H = H;
+  p.d = d;
+  p.head_stride_rows = Ts;  // scratch means [H][Ts] (a by-product; the packer recomputes them)
+  p.status = status;
+  p.mode = k_smoothing ? kModeSmoothK : 0;
+  p.mean_out = reinterpret_cast<float*>(sc + 2 * kNumPartials * sizeof(uint32_t) + 64);
+  p.partials_w = partials;
+  return cuda_status(launch_ulysses_shard_amax(p, partials, dev_amax_kv, S(stream)));
+}
+
+kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, kvq_dtype dtype, int32_t Ts, int32_t H,
+                                  int32_t d, int32_t P, const float* dev_amax_kv, int32_t scale_mode,
+                                  int32_t k_smoothing, void* send_buf, void* stream) {
+  if (!Q || !K || !V || !dev_amax_kv || !send_buf || Ts <= 0 || H <= 0 || H > 256 || P <= 0 || P > kMaxP)
+    return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if ((scale_mode != 0 && scale_mode != 1) || (k_smoothing != 0 && k_smoothing != 1)) return KVQ_EINVAL;
+  PackNvfp4Params p{};
+  p.x[0] = Q;
+  p.x[1] = K;
+  p.x[2] = V;
+  p.dtype = dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.Ts = Ts;
+  p.H = H;
+  p.d = d;
+  p.P = P;
+  p.mode = (scale_mode == 1 ? kModeSearch : 0) | (k_smoothing ? kModeSmoothK : 0);
+  p.amax = dev_amax_kv;
+  p.send = static_cast<uint8_t*>(send_buf);
+  ulysses_partition(H, P, p.h0, p.owner);
+  int64_t off = 0;
+  for (int r = 0; r < P; ++r) {
+    p.seg_off[r] = off;
+    p.lay[r] = nvfp4_seg_layout(Ts, p.h0[r + 1] - p.h0[r], d, (int)esize(dtype), k_smoothing != 0);
+    off += p.lay[r].total;
+  }
+  return cuda_status(launch_ulysses_pack_nvfp4(p, S(stream)));
+}
+
+kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_index, const void* recv_buf, int32_t P,
+                                   const float* dev_amax_kv, void* Q_out, kvq_dtype q_dtype, void* stream) {
+  if (!c || !recv_buf || !dev_amax_kv || !Q_out || P <= 0 || P > kMaxP) return KVQ_EINVAL;
+  if (layer < 0 || layer >= c->cfg.num_layers || chunk_index < 0) return KVQ_EINVAL;
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (c->L.T_c % P) return KVQ_ESHAPE;
+  int slot = -1;
+  const kvq_status ss = select_slot(c, layer, chunk_index, &slot);
+  if (ss != KVQ_OK) return ss;
+  const int Hr = c->cfg.num_heads, d = c->cfg.head_dim, Ts = (int)(c->L.T_c / P);
+  ScatterNvfp4Params p{};
+  p.recv = static_cast<const uint8_t*>(recv_buf);
+  p.lay = nvfp4_seg_layout(Ts, Hr, d, (int)esize(q_dtype), c->cfg.k_smoothing != 0);
+  p.seg = p.lay.total;
+  p.Ts = Ts;
+  p.Hr = Hr;
+  p.d = d;
+  p.es = (int)esize(q_dtype);
+  p.P = P;
+  for (int t = 0; t < 2; ++t) {
+    p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
+    p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);
+  }
+  p.mean = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
+  p.head_stride_rows = c->L.rows_per_head;
+  p.Q = Q_out;
+  p.amax = dev_amax_kv;
+  p.g_out = g_base(c, layer) + slot * 2;
+  p.status = status_ptr(c);
+  if (launch_ulysses_scatter_nvfp4(p, S(stream)) != cudaSuccess) return KVQ_ECUDA;
+  commit_slot(c, layer, chunk_index, slot);
+  return KVQ_OK;
 }
 
 kvq_status kvq_debug_force_two_pass(kvq_cache* c, int32_t on) {

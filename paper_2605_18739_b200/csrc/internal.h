@@ -126,6 +126,56 @@ cudaError_t launch_ulysses_unpack_qkv(const uint8_t* recv, int dtype, int Ts, in
 cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int H, int d, int P, void* O,
                                     cudaStream_t st);
 
+// NVFP4 payload exchange (§8(f) f3): layout of one destination segment built
+// from a source shard of Ts tokens for a destination owning Hp heads, rows (t, h_local) t-major:
+// [Q Ts*Hp*d*es][K codes Ts*Hp*d/2][K scales Ts*Hp*d/16][V codes][V scales][K means Ts*Hp*4 if
+// smoothing], every part padded to 16 bytes.
+constexpr int kMaxP = 64;
+struct Nvfp4SegLayout {
+  int64_t q, kc, ks, vc, vs, km, total;  // byte offsets within the segment, total size
+};
+inline int64_t pad16(int64_t x) { return (x + 15) & ~int64_t(15); }
+inline Nvfp4SegLayout nvfp4_seg_layout(int Ts, int Hp, int d, int es, bool smooth) {
+  Nvfp4SegLayout L{};
+  const int64_t rows = (int64_t)Ts * Hp;
+  L.q = 0;
+  L.kc = pad16(rows * d * es);
+  L.ks = L.kc + pad16(rows * d / 2);
+  L.vc = L.ks + pad16(rows * d / 16);
+  L.vs = L.vc + pad16(rows * d / 2);
+  L.km = L.vs + pad16(rows * d / 16);
+  L.total = L.km + (smooth ? pad16(rows * 4) : 0);
+  return L;
+}
+struct PackNvfp4Params {
+  const void* x[3];          // Q, K, V shards [Ts, H, d] (dtype)
+  int dtype, Ts, H, d, P, mode;
+  const float* amax;         // [2] global amax of K (K_bar with smoothing) and V over all ranks
+  uint8_t* send;
+  int64_t seg_off[kMaxP];    // byte offset of destination r's segment
+  Nvfp4SegLayout lay[kMaxP];  // its layout
+  int h0[kMaxP + 1];
+  uint8_t owner[256];
+};
+struct ScatterNvfp4Params {
+  const uint8_t* recv;       // P segments of equal size (this rank is every source's destination)
+  Nvfp4SegLayout lay;
+  int64_t seg;               // segment stride in bytes
+  int Ts, Hr, d, es, P;
+  uint8_t* codes[2];         // cache slot bases (head 0), head-major rows of d/2 bytes
+  uint8_t* scales[2];
+  float* mean;               // K-smoothing row means of the slot (head 0) or null
+  int64_t head_stride_rows;
+  void* Q;                   // out: [P*Ts, Hr, d] (dtype)
+  const float* amax;         // [2] global amax -> g of the slot
+  float* g_out;
+  DevStatus* status;
+};
+cudaError_t launch_ulysses_shard_amax(const QuantParams& p, uint32_t* partials, float* amax_out, cudaStream_t st);
+cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st);
+cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st);
+void ulysses_partition(int H, int P, int* h0, uint8_t* owner);
+
 // Debug probes (codec checks against the oracle)
 cudaError_t launch_probe(int which, const void* in, void* out, int64_t n, cudaStream_t st);
 

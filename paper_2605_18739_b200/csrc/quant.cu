@@ -940,6 +940,100 @@ __global__ void __launch_bounds__(kSpThreads, 1)
 
 #undef SPTRACE
 
+// ---------------------------------------------------------------------------------------------
+// NVFP4 payload for the Ulysses exchange (§8(f) f3; App. D: the all-to-all
+// "performed entirely in the low-precision space").  The sender quantizes its sequence shard of K
+// and V with the GLOBAL tensor scales (amax all-reduced over the ranks first, readings Z2/Z18), so
+// the packed bytes it ships are exactly the bytes the 1-GPU cache holds for those rows: blocks run
+// along d inside one (t, h) row, and rows never straddle ranks.  Q travels in its input dtype.
+
+// reduce the per-CTA partials of amax_kernel / smooth_amax_kernel to the shard's [K, V] amax
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const uint32_t* partials, float* amax_out) {
+  __shared__ uint32_t red[2][8];
+  for (int t = 0; t < 2; ++t) {
+    uint32_t m = 0;
+    for (int k = threadIdx.x; k < kNumPartials; k += blockDim.x) m = max(m, partials[t * kNumPartials + k]);
+    m = warp_max_u32(m);
+    if ((threadIdx.x & 31) == 0) red[t][threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    uint32_t m = 0;
+    for (int w = 0; w < 8; ++w) m = max(m, red[threadIdx.x][w]);
+    amax_out[threadIdx.x] = __uint_as_float(m);  // bits of max |x| (inf/NaN bits stay non-finite)
+  }
+}
+
+// One thread per 16-element block of K or V of the shard, blocks (t, h, j) with j fastest, so the
+// d/16 blocks of a row sit in consecutive lanes (K-smoothing's row mean is a lane butterfly).
+template <int DT, int D, int MODE>
+__global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__ PackNvfp4Params p) {
+  constexpr bool SEARCH = (MODE & kModeSearch) != 0;
+  constexpr bool SMOOTH = (MODE & kModeSmoothK) != 0;
+  constexpr int kNB = D / 16;
+  constexpr int kUB = 16 * (DT == DT_BF16 ? 2 : 4);
+  constexpr int es = DT == DT_BF16 ? 2 : 4;
+  const int64_t nblk = (int64_t)p.Ts * p.H * kNB;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // ---- Q rows, passed through (16-byte chunks)
+  {
+    constexpr int cpr = D * es / 16;
+    const int64_t total = (int64_t)p.Ts * p.H * cpr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int64_t row = i / cpr;
+      const int cc = (int)(i - row * cpr);
+      const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+      const int r = p.owner[h];
+      const int Hp = p.h0[r + 1] - p.h0[r];
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>((const uint8_t*)p.x[0] + row * D * es) + cc);
+      uint8_t* o = p.send + p.seg_off[r] + p.lay[r].q + ((int64_t)t * Hp + (h - p.h0[r])) * D * es;
+      reinterpret_cast<uint4*>(o)[cc] = v;
+    }
+  }
+  // ---- K, V blocks -> codes + scale bytes (+ K row means) in the destination's segment
+  for (int t = 0; t < 2; ++t) {
+    const bool smooth_t = SMOOTH && t == 0;
+    const uint32_t abits = __float_as_uint(p.amax[t]) & 0x7FFFFFFFu;
+    if (abits >= 0x7F800000u) continue;  // non-finite: the receiver reports it, bytes undefined
+    const float amax = __uint_as_float(abits);
+    const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
+    const float rg = __frcp_rn(g);
+    const bool exact = !(g >= 0x1p-60f && g <= 0x1p60f);
+    const uint8_t* x = (const uint8_t*)p.x[1 + t];
+    // warp-uniform trip count (the row butterfly needs every lane)
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nblk; base += stride) {
+      const int64_t u = base + (threadIdx.x & 31);
+      const bool valid = u < nblk;
+      float v[1][16];
+      if (valid) {
+        unpack_block16<DT>(x + u * kUB, v[0]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[0][e] = 0.0f;
+      }
+      float mean = 0.0f;
+      if (smooth_t) {
+        mean = row_mean<kNB>(v[0]);
+        subtract_mean(v[0], mean);
+      }
+      if (!valid) continue;
+      uint32_t sb[1], w0[1], w1[1];
+      const uint32_t flags = exact ? 1u : quantize_blocks_fast<1, SEARCH>(v, g, rg, sb, w0, w1);
+      if (flags) quantize_block16_exact<SEARCH>(v[0], g, sb[0], w0[0], w1[0]);
+      const int64_t row = u / kNB;
+      const int j = (int)(u - row * kNB);
+      const int tt = (int)(row / p.H), h = (int)(row - (int64_t)tt * p.H);
+      const int r = p.owner[h];
+      const int Hp = p.h0[r + 1] - p.h0[r];
+      const int64_t orow = (int64_t)tt * Hp + (h - p.h0[r]);
+      uint8_t* seg = p.send + p.seg_off[r];
+      *reinterpret_cast<uint2*>(seg + (t ? p.lay[r].vc : p.lay[r].kc) + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
+      seg[(t ? p.lay[r].vs : p.lay[r].ks) + orow * kNB + j] = (uint8_t)sb[0];
+      if (smooth_t && j == 0) reinterpret_cast<float*>(seg + p.lay[r].km)[orow] = mean;
+    }
+  }
+}
+
 // Eq. 2: x^ = dec(c) dec(s) g.  dec(c) dec(s) is exact in fp32 (<= 7 significant
 // bits), so one FMA with g (and the K-smoothing row mean, else -0) rounds the exact value once.
 template <int D>
@@ -1214,6 +1308,36 @@ cudaError_t launch_dequant_window(const DequantParams& base, const AttnSeg* segs
   if (p.d == 128) dequant_window_kernel<128><<<grid, 256, 0, st>>>(p, base.g, ws);
   else dequant_window_kernel<64><<<grid, 256, 0, st>>>(p, base.g, ws);
   return cudaGetLastError();
+}
+
+cudaError_t launch_ulysses_shard_amax(const QuantParams& p, uint32_t* partials, float* amax_out, cudaStream_t st) {
+  cudaError_t e;
+  if (p.mode & kModeSmoothK) {  // K_bar partials (means to p.mean_out), then V's
+    e = launch_smooth_amax(p, st);
+    if (e == cudaSuccess) e = launch_amax(p.x[0], p.x[1], p.dtype, (int64_t)p.rows * p.d, partials, p.status, st, 1);
+  } else {
+    e = launch_amax(p.x[0], p.x[1], p.dtype, (int64_t)p.rows * p.d, partials, p.status, st);
+  }
+  if (e != cudaSuccess) return e;
+  reduce_partials_kernel<<<1, 256, 0, st>>>(partials, amax_out);
+  return cudaGetLastError();
+}
+
+template <int DT, int D>
+cudaError_t pack_nvfp4_mode(const PackNvfp4Params& p, int grid, cudaStream_t st) {
+  switch (p.mode & 3) {
+    case 0: pack_nvfp4_kernel<DT, D, 0><<<grid, 256, 0, st>>>(p); break;
+    case 1: pack_nvfp4_kernel<DT, D, 1><<<grid, 256, 0, st>>>(p); break;
+    case 2: pack_nvfp4_kernel<DT, D, 2><<<grid, 256, 0, st>>>(p); break;
+    default: pack_nvfp4_kernel<DT, D, 3><<<grid, 256, 0, st>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st) {
+  const int grid = grid_for((int64_t)p.Ts * p.H * (p.d / 16), 256);
+  if (p.dtype == DT_BF16) return p.d == 128 ? pack_nvfp4_mode<DT_BF16, 128>(p, grid, st) : pack_nvfp4_mode<DT_BF16, 64>(p, grid, st);
+  return p.d == 128 ? pack_nvfp4_mode<DT_FP32, 128>(p, grid, st) : pack_nvfp4_mode<DT_FP32, 64>(p, grid, st);
 }
 
 cudaError_t launch_probe(int which, const void* in, void* out, int64_t n, cudaStream_t st) {

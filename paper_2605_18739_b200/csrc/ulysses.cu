@@ -10,8 +10,6 @@
 namespace kvq {
 namespace {
 
-constexpr int kMaxP = 64;
-
 struct PackParams {
   const uint8_t* x[3];
   uint8_t* send;
@@ -108,12 +106,61 @@ __global__ void __launch_bounds__(256) unpack_o_kernel(const __grid_constant__ U
   }
 }
 
+// NVFP4 exchange, receiving side: every source segment carries Ts tokens of this rank's Hr heads
+// as Q rows, packed K/V codes + scale bytes (+ K means): scatter them into the cache slot
+// (head-major rows h * head_stride_rows + src * Ts + t) and Q into [P*Ts, Hr, d]; g of the slot
+// from the all-reduced amax (the sender quantized with the same g).
+__global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constant__ ScatterNvfp4Params p) {
+  const int64_t rows = (int64_t)p.Ts * p.Hr;      // per source
+  const int qc = p.d * p.es / 16, cc = p.d / 2 / 16;  // 16-byte chunks per Q row, per code row
+  const int64_t per_src = rows * (qc + 2 * cc);
+  const int64_t total = (int64_t)p.P * per_src;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int src = (int)(i / per_src);
+    int64_t r = i - src * per_src;
+    const uint8_t* seg = p.recv + src * p.seg;
+    if (r < rows * qc) {  // Q chunk
+      const int64_t row = r / qc;
+      const int c = (int)(r - row * qc);
+      const int t = (int)(row / p.Hr), h = (int)(row - (int64_t)t * p.Hr);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + row * p.d * p.es) + c);
+      reinterpret_cast<uint4*>((uint8_t*)p.Q + (((int64_t)src * p.Ts + t) * p.Hr + h) * p.d * p.es)[c] = v;
+      continue;
+    }
+    r -= rows * qc;
+    const int tsr = (int)(r / (rows * cc));
+    r -= (int64_t)tsr * rows * cc;
+    const int64_t row = r / cc;
+    const int c = (int)(r - row * cc);
+    const int t = (int)(row / p.Hr), h = (int)(row - (int64_t)t * p.Hr);
+    const int64_t orow = (int64_t)h * p.head_stride_rows + (int64_t)src * p.Ts + t;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + (tsr ? p.lay.vc : p.lay.kc) + row * (p.d / 2)) + c);
+    reinterpret_cast<uint4*>(p.codes[tsr] + orow * (p.d / 2))[c] = v;
+    if (c == 0) {  // the row's scale bytes (d/16) and K mean
+      const uint8_t* sc = seg + (tsr ? p.lay.vs : p.lay.ks) + row * (p.d / 16);
+      uint8_t* dst = p.scales[tsr] + orow * (p.d / 16);
+      if (p.d == 128) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(sc);
+      else *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(sc);
+      if (tsr == 0 && p.mean) p.mean[orow] = reinterpret_cast<const float*>(seg + p.lay.km)[row];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2) {
+    const uint32_t abits = __float_as_uint(p.amax[threadIdx.x]) & 0x7FFFFFFFu;
+    if (abits >= 0x7F800000u) {
+      atomicCAS(&p.status->code, 0, -6);
+    } else {
+      const float amax = __uint_as_float(abits);
+      p.g_out[threadIdx.x] = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
+    }
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t g = (work + 255) / 256;
   return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
 }
 
-void partition(int H, int P, int* h0, uint8_t* owner) {
+void partition_impl(int H, int P, int* h0, uint8_t* owner) {
   const int base = H / P, rem = H % P;
   h0[0] = 0;
   for (int r = 0; r < P; ++r) h0[r + 1] = h0[r] + base + (r < rem ? 1 : 0);
@@ -122,6 +169,14 @@ void partition(int H, int P, int* h0, uint8_t* owner) {
 }
 
 }  // namespace
+
+void ulysses_partition(int H, int P, int* h0, uint8_t* owner) { partition_impl(H, P, h0, owner); }
+
+cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st) {
+  const int64_t work = (int64_t)p.P * p.Ts * p.Hr * (p.d * p.es / 16 + p.d / 16);
+  scatter_nvfp4_kernel<<<grid_for(work), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int dtype, int Ts, int H, int d, int P,
                                 uint8_t* send, uint32_t* scratch, cudaStream_t st) {
@@ -135,7 +190,7 @@ cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int
   p.x[2] = (const uint8_t*)V;
   p.send = send;
   p.partials = scratch;
-  partition(H, P, p.h0, p.owner);
+  partition_impl(H, P, p.h0, p.owner);
   int64_t off = 0;
   for (int r = 0; r < P; ++r) {
     p.seg_off[r] = off;
@@ -165,7 +220,7 @@ cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int 
   UnpackOParams p{};
   p.recv = recv;
   p.out = (uint8_t*)O;
-  partition(H, P, p.h0, p.owner);
+  partition_impl(H, P, p.h0, p.owner);
   int64_t off = 0;
   for (int r = 0; r < P; ++r) {
     p.src_off[r] = off;

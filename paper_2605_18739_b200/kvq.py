@@ -86,6 +86,14 @@ _SIGS = {
                                               ctypes.c_int32, _P, _P, _P, _P, _P]),
     "kvq_ulysses_unpack_o": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, _P, _P]),
+    "kvq_ulysses_shard_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "kvq_ulysses_nvfp4_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 5 + [ctypes.c_int, ctypes.c_int32]),
+    "kvq_ulysses_shard_amax": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, _P, _P, _P]),
+    "kvq_ulysses_pack_nvfp4": (ctypes.c_int, [_P, _P, _P, ctypes.c_int] + [ctypes.c_int32] * 4 +
+                               [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
+    "kv_append_ulysses_nvfp4": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, ctypes.c_int32, _P, _P,
+                                               ctypes.c_int, _P]),
     "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
     "kvq_debug_set_trace": (ctypes.c_int, [_P]),
     "kvq_debug_force_two_pass": (ctypes.c_int, [_P, ctypes.c_int32]),
@@ -208,6 +216,14 @@ class KVCache:
                                      _out_code(out.dtype), _stream()), "chunk_attention")
         return out
 
+    def append_ulysses_nvfp4(self, layer, chunk_index, recv, P, amax_kv, q_dtype=torch.bfloat16, Q_out=None):
+        """kv_append_ulysses_nvfp4: the P received NVFP4 segments become chunk `chunk_index`; returns Q."""
+        if Q_out is None:
+            Q_out = torch.empty((self.T_c, self.H, self.d), dtype=q_dtype, device=self.device)
+        _check(lib().kv_append_ulysses_nvfp4(self._h, layer, chunk_index, _ptr(recv), P, _ptr(amax_kv), _ptr(Q_out),
+                                             _out_code(Q_out.dtype), _stream()), "kv_append_ulysses_nvfp4")
+        return Q_out
+
     def dequantize(self, layer, chunk_index, out_dtype=torch.float32):
         K = torch.empty((self.T_c, self.H, self.d), dtype=out_dtype, device=self.device)
         V = torch.empty_like(K)
@@ -324,6 +340,34 @@ def ulysses_unpack_o(recv, Ts, H, d, P, dtype=torch.bfloat16, out=None):
     return out
 
 
+def ulysses_nvfp4_bytes(Ts, H, d, P, dst, q_dtype=torch.bfloat16, k_smoothing=False):
+    return int(lib().kvq_ulysses_nvfp4_bytes(Ts, H, d, P, dst, _out_code(q_dtype), int(k_smoothing)))
+
+
+def ulysses_shard_amax(K, V, k_smoothing=False, out=None, scratch=None):
+    """kvq_ulysses_shard_amax: [max |K| (|K - row mean| with smoothing), max |V|] of this rank's shard."""
+    Ts, H, d = K.shape
+    if out is None:
+        out = torch.empty(2, dtype=torch.float32, device=K.device)
+    if scratch is None:
+        scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(Ts, H)), dtype=torch.uint8, device=K.device)
+    _check(lib().kvq_ulysses_shard_amax(_ptr(K), _ptr(V), _dt(K), Ts, H, d, int(k_smoothing), _ptr(out),
+                                        _ptr(scratch), _stream()), "kvq_ulysses_shard_amax")
+    return out
+
+
+def ulysses_pack_nvfp4(Q, K, V, P, amax_kv, scale_search=False, k_smoothing=False, send=None):
+    """kvq_ulysses_pack_nvfp4: shard -> send buffer with K/V as NVFP4 under the GLOBAL amax_kv."""
+    Ts, H, d = Q.shape
+    sizes = [ulysses_nvfp4_bytes(Ts, H, d, P, p, Q.dtype, k_smoothing) for p in range(P)]
+    if send is None:
+        send = torch.empty(sum(sizes), dtype=torch.uint8, device=Q.device)
+    _check(lib().kvq_ulysses_pack_nvfp4(_ptr(Q), _ptr(K), _ptr(V), _dt(Q), Ts, H, d, P, _ptr(amax_kv),
+                                        int(bool(scale_search)), int(bool(k_smoothing)), _ptr(send), _stream()),
+           "kvq_ulysses_pack_nvfp4")
+    return send, sizes
+
+
 class Ulysses:
     """Head-sharded chunk step of one rank (App. C; App. D).
 
@@ -332,7 +376,9 @@ class Ulysses:
     of O (NCCL) -> head interleave (kernel).
     """
 
-    def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16):
+    def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16, nvfp4_kv=False):
+        """nvfp4_kv (§8(f) f3): ship K/V as NVFP4 bytes quantized on the sender with
+        the all-reduced global amax (one extra tiny NCCL all-reduce; ~3.6x less K/V volume)."""
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.cache, self.H, self.d, self.T_c = cache, H, d, T_c
@@ -361,11 +407,30 @@ class Ulysses:
                              for p in range(world)]
         self.o_recv = torch.empty(sum(self.o_recv_sizes), dtype=torch.uint8, device=dev)
         self.es = es
+        # K-smoothing needs the amax of K_bar, which the bf16 exchange's piggybacked shard amax is not
+        self.nvfp4_kv = bool(nvfp4_kv) or cache.k_smoothing
+        if self.nvfp4_kv:
+            sm = cache.k_smoothing
+            self.nv_send_sizes = [ulysses_nvfp4_bytes(self.Ts, H, d, world, p, dtype, sm) for p in range(world)]
+            self.nv_recv_seg = ulysses_nvfp4_bytes(self.Ts, H, d, world, rank, dtype, sm)
+            self.nv_send = torch.empty(sum(self.nv_send_sizes), dtype=torch.uint8, device=dev)
+            self.nv_recv = torch.empty(self.nv_recv_seg * world, dtype=torch.uint8, device=dev)
+            self.amax_scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(self.Ts, H)), dtype=torch.uint8,
+                                            device=dev)
 
     def step(self, layer, chunk_index, Q, K, V, mask: Mask, out=None):
         """One layer of one chunk: Q, K, V are this rank's sequence shards [T_c/P, H, d]."""
         L, st = lib(), _stream()
         dt = _dt(Q)
+        if self.nvfp4_kv:
+            c = self.cache
+            ulysses_shard_amax(K, V, c.k_smoothing, out=self.amax, scratch=self.amax_scratch)
+            self.dist.all_reduce(self.amax, op=self.dist.ReduceOp.MAX, group=self.group)
+            ulysses_pack_nvfp4(Q, K, V, self.P, self.amax, c.scale_search, c.k_smoothing, send=self.nv_send)
+            self.dist.all_to_all_single(self.nv_recv, self.nv_send, output_split_sizes=[self.nv_recv_seg] * self.P,
+                                        input_split_sizes=self.nv_send_sizes, group=self.group)
+            c.append_ulysses_nvfp4(layer, chunk_index, self.nv_recv, self.P, self.amax, Q_out=self.Q)
+            return self._attend_and_return(layer, mask, out, Q)
         _check(L.kvq_ulysses_pack_qkv(_ptr(Q), _ptr(K), _ptr(V), dt, self.Ts, self.H, self.d, self.P,
                                       _ptr(self.send), _ptr(self.scratch), st), "kvq_ulysses_pack_qkv")
         self.dist.all_to_all_single(self.recv, self.send, output_split_sizes=[self.recv_seg] * self.P,
@@ -373,6 +438,10 @@ class Ulysses:
         _check(L.kvq_ulysses_unpack_qkv(_ptr(self.recv), dt, self.Ts, self.Hr, self.d, self.P, _ptr(self.Q),
                                         _ptr(self.K), _ptr(self.V), _ptr(self.amax), st), "kvq_ulysses_unpack_qkv")
         self.cache.append(layer, chunk_index, self.K, self.V, amax_kv=self.amax)
+        return self._attend_and_return(layer, mask, out, Q)
+
+    def _attend_and_return(self, layer, mask, out, Q):
+        L, st = lib(), _stream()
         self.cache.attention(layer, self.Q, mask, out=self.O_local)
         o_send = self.O_local.view(torch.uint8).reshape(-1)
         self.dist.all_to_all_single(self.o_recv, o_send, output_split_sizes=self.o_recv_sizes,

@@ -89,3 +89,55 @@ def test_pack_trailer_carries_shard_amax():
         tr = send[off + sz - 16: off + sz].view(torch.float32)
         assert tr[0].item() == K.float().abs().max().item() and tr[1].item() == V.float().abs().max().item()
         off += sz
+
+
+@pytest.mark.parametrize("P,H,search,smooth", [(2, 12, False, False), (4, 12, False, False), (8, 12, False, False),
+                                               (8, 24, False, False), (3, 7, False, False), (4, 12, True, False),
+                                               (4, 12, False, True), (8, 12, True, True)])
+def test_ulysses_nvfp4_exchange_simulated_matches_single_gpu(P, H, search, smooth):
+    # §8(f) f3: K/V cross the all-to-all as NVFP4 bytes quantized on the sender
+    # under the all-reduced global amax; each rank's cache must hold exactly the 1-GPU bytes of its heads
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d = 40, 3, 128
+    T = tpf * fc
+    Ts = T // P
+    sink, window = 3, 9
+    parts = [kvq.head_partition(H, P, r) for r in range(P)]
+    mk = dict(sink_frames=sink, window_frames=window, max_chunk_slots=8, device=DEV, scale_search=search,
+              k_smoothing=smooth)
+    caches = [kvq.KVCache(1, h1 - h0, d, tpf, fc, **mk) for h0, h1 in parts]
+    ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    orc = OracleKVCache(1, H, d, tpf, fc, scale_search=search, k_smoothing=smooth)
+    for ch in range(5):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch, variant="outlier" if ch % 2 else "iid")
+        Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+        mask = kvq.Mask(ch, sink, window)
+        ref.append(0, ch, K, V)
+        O_ref = ref.attention(0, Q, mask, torch.float32)
+        orc.append(0, ch, k.f64, v.f64)
+        shards = [tuple(x[r * Ts:(r + 1) * Ts].contiguous() for x in (Q, K, V)) for r in range(P)]
+        amax = torch.stack([kvq.ulysses_shard_amax(Kr, Vr, smooth) for _, Kr, Vr in shards]).max(0).values  # all-reduce
+        packed = [kvq.ulysses_pack_nvfp4(Qr, Kr, Vr, P, amax, search, smooth) for Qr, Kr, Vr in shards]
+        recv = _a2a([sd for sd, _ in packed], [sz for _, sz in packed], None)
+        O_locals = []
+        for p, (h0, h1) in enumerate(parts):
+            Ql = caches[p].append_ulysses_nvfp4(0, ch, recv[p], P, amax)
+            assert torch.equal(Ql, Q[:, h0:h1])
+            O_locals.append(caches[p].attention(0, Ql, mask, torch.float32))
+        o_bytes = [[Ts * (h1 - h0) * d * 4 for _ in range(P)] for h0, h1 in parts]
+        o_recv = _a2a([o.view(torch.uint8).reshape(-1) for o in O_locals], o_bytes, None)
+        O_full = torch.cat([kvq.ulysses_unpack_o(o_recv[r], Ts, H, d, P, torch.float32) for r in range(P)])
+        ex = ref.export(0, ch)
+        for p, (h0, h1) in enumerate(parts):
+            e = caches[p].export(0, ch)
+            for name in ("codes_k", "scales_k", "codes_v", "scales_v"):
+                full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
+                assert torch.equal(e[name], full), (p, name)
+            assert torch.equal(e["g_k"], ex["g_k"]) and torch.equal(e["g_v"], ex["g_v"])
+            if smooth:
+                km = ref.export_kmean(0, ch).view(T, H)[:, h0:h1].reshape(-1)
+                assert torch.equal(caches[p].export_kmean(0, ch), km)
+        assert torch.allclose(O_full, O_ref, rtol=1e-3, atol=2e-4)
+        check_fp32_out(O_full.cpu().numpy(), orc.attend(0, ch, q.f64, sink, window))
+
