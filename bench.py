@@ -171,7 +171,8 @@ def run_gpu(args):
         q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, ch)
         chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
     dq = [tuple(x.to(dev) for x in c) for c in chunks]
-    uly = kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4") if P > 1 else None
+    uly = (kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer")
+           if P > 1 else None)
 
     def step(c, out=None):
         q, k, v = dq[c]
@@ -306,8 +307,10 @@ def run_gpu(args):
                       "exchange": args.exchange if world > 1 else None,
                       "l2": "flushed (256 MiB write) before every timed step"},
            # per step: N=1 quantize/append (1) + attention (1) + split-KV combine (1);
-           # N>1 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted)
-           "gpu_launches": args.steps * (3 if world == 1 else 7)}
+           # N>1 bf16 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted); nvfp4: amax (2-3),
+           # reduce, pack, scatter, attention + combine, unpack O; peer: amax (2-3), reduce, publish, pack, scatter,
+           # attention + combine, signal, pull
+           "gpu_launches": args.steps * (3 if world == 1 else {"bf16": 7, "nvfp4": 8, "peer": 10}[args.exchange])}
     if uly is None:
         att_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_att]))
         app_ms_ev = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
@@ -423,8 +426,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
-    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4"],
-                    help="N>1: K/V payload of the all-to-all (nvfp4 = §8(f) f3, quantized on the sender)")
+    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "peer"],
+                    help="N>1: bf16 all-to-all (NCCL), nvfp4 = §8(f) f3 (K/V quantized on the sender, NCCL), "
+                         "peer = §8(f) f4 (the kernels store/load over NVLink peer memory, no NCCL on the data path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -250,6 +250,45 @@ kvq_status kv_append_ulysses_nvfp4(kvq_cache* cache, int32_t layer, int64_t chun
                                    const void* recv_buf, int32_t P, const float* dev_amax_kv,
                                    void* Q_out, kvq_dtype q_dtype, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Device-initiated exchange over peer memory (§8(f) f4): the NVFP4 exchange above without NCCL.
+ * Every rank owns one "window" of kvq_peer_window_bytes (identical layout on all ranks, sized for
+ * the largest head share): P receive segments, a mailbox of P shard amaxes, P arrival counters, P
+ * O-ready flags and two O_local buffers.  `windows` are the P ranks' window base pointers as seen
+ * from this rank -- peer pointers over NVLink/NVSwitch (e.g. torch symmetric memory), or plain
+ * device pointers when P ranks are simulated on one GPU.  The caller zeroes every window once.
+ * Per step (epoch = 1, 2, 3, ... consecutively, < 2^32), on each rank's stream:
+ *   kvq_peer_publish_amax  shard amax -> every peer's mailbox (st.release.sys)
+ *   kvq_peer_pack          waits for its mailbox (all P), quantizes its shard with the global scale
+ *                          and stores each destination's rows straight into that rank's window,
+ *                          then bumps the destination's arrival counter (fence.sys + red.release.sys)
+ *   kv_append_peer         waits for all P arrivals, scatters into the cache slot (append policy)
+ *   chunk_attention        on the local heads, O into kvq_peer_o_local(epoch)
+ *   kvq_peer_signal_o      O-ready flag -> every peer
+ *   kvq_peer_pull_o        waits for all P flags, pulls this rank's token rows of every head.
+ * Waits are device-side spins: all ranks must run the same sequence of steps. */
+typedef struct kvq_peer kvq_peer;
+size_t kvq_peer_window_bytes(int32_t T_c, int32_t H, int32_t d, int32_t P, kvq_dtype q_dtype,
+                             int32_t k_smoothing);
+kvq_status kvq_peer_create(int32_t T_c, int32_t H, int32_t d, int32_t P, int32_t rank,
+                           kvq_dtype q_dtype, int32_t scale_mode, int32_t k_smoothing,
+                           void* const* windows, kvq_peer** out);
+kvq_status kvq_peer_destroy(kvq_peer* peer);
+/* O_local dev [T_c, H_rank, d] bf16 of this rank for `epoch` (alternating buffers). */
+kvq_status kvq_peer_o_local(const kvq_peer* peer, int64_t epoch, void** out);
+/* dev_scratch >= kvq_ulysses_shard_scratch_bytes(T_c/P, H) + 16 bytes. */
+kvq_status kvq_peer_publish_amax(const kvq_peer* peer, const void* K_shard, const void* V_shard,
+                                 int64_t epoch, void* dev_scratch, void* stream);
+kvq_status kvq_peer_pack(const kvq_peer* peer, const void* Q_shard, const void* K_shard,
+                         const void* V_shard, int64_t epoch, void* stream);
+/* cache: this rank's heads, same d / T_c / modes as the peer config (else KVQ_ESHAPE).
+ * Q_out dev [T_c, H_rank, d] (q_dtype). */
+kvq_status kv_append_peer(const kvq_peer* peer, kvq_cache* cache, int32_t layer,
+                          int64_t chunk_index, int64_t epoch, void* Q_out, void* stream);
+kvq_status kvq_peer_signal_o(const kvq_peer* peer, int64_t epoch, void* stream);
+/* O_shard dev [T_c/P, H, d] bf16. */
+kvq_status kvq_peer_pull_o(const kvq_peer* peer, int64_t epoch, void* O_shard, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -696,6 +696,186 @@ kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_in
   return KVQ_OK;
 }
 
+// ---- Device-initiated exchange over peer memory (§8(f) f4)
+struct PeerWindowLayout {
+  int64_t recv, seg, mailbox, arrive, flags, o[2], total;
+};
+static PeerWindowLayout peer_layout(int32_t T_c, int32_t H, int32_t d, int32_t P, kvq_dtype q_dtype,
+                                    int32_t k_smoothing) {
+  PeerWindowLayout L{};
+  const int Ts = T_c / P, hmax = (H + P - 1) / P;
+  auto a128 = [](int64_t x) { return (x + 127) & ~int64_t(127); };
+  L.seg = nvfp4_seg_layout(Ts, hmax, d, (int)esize(q_dtype), k_smoothing != 0).total;
+  L.recv = 0;
+  L.mailbox = a128(P * L.seg);
+  L.arrive = L.mailbox + a128(16 * (int64_t)P);
+  L.flags = L.arrive + a128(8 * (int64_t)P);
+  L.o[0] = L.flags + a128(8 * (int64_t)P);
+  L.o[1] = L.o[0] + a128((int64_t)T_c * hmax * d * 2);
+  L.total = L.o[1] + a128((int64_t)T_c * hmax * d * 2);
+  return L;
+}
+
+struct kvq_peer {
+  int32_t T_c, H, d, P, rank, scale_mode, k_smoothing;
+  kvq_dtype q_dtype;
+  PeerWindowLayout L;
+  uint8_t* win[kMaxP];
+};
+
+size_t kvq_peer_window_bytes(int32_t T_c, int32_t H, int32_t d, int32_t P, kvq_dtype q_dtype, int32_t k_smoothing) {
+  if (P <= 0 || P > kMaxP || T_c <= 0 || T_c % P) return 0;
+  return (size_t)peer_layout(T_c, H, d, P, q_dtype, k_smoothing).total;
+}
+
+kvq_status kvq_peer_create(int32_t T_c, int32_t H, int32_t d, int32_t P, int32_t rank, kvq_dtype q_dtype,
+                           int32_t scale_mode, int32_t k_smoothing, void* const* windows, kvq_peer** out) {
+  if (!windows || !out || P <= 0 || P > kMaxP || rank < 0 || rank >= P || H <= 0 || H > 256 || T_c <= 0)
+    return KVQ_EINVAL;
+  if (T_c % P) return KVQ_ESHAPE;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if ((scale_mode != 0 && scale_mode != 1) || (k_smoothing != 0 && k_smoothing != 1)) return KVQ_EINVAL;
+  kvq_peer* pe = new kvq_peer{};
+  pe->T_c = T_c;
+  pe->H = H;
+  pe->d = d;
+  pe->P = P;
+  pe->rank = rank;
+  pe->q_dtype = q_dtype;
+  pe->scale_mode = scale_mode;
+  pe->k_smoothing = k_smoothing;
+  pe->L = peer_layout(T_c, H, d, P, q_dtype, k_smoothing);
+  for (int r = 0; r < P; ++r) {
+    if (!windows[r]) {
+      delete pe;
+      return KVQ_EINVAL;
+    }
+    pe->win[r] = static_cast<uint8_t*>(windows[r]);
+  }
+  *out = pe;
+  return KVQ_OK;
+}
+
+kvq_status kvq_peer_destroy(kvq_peer* pe) {
+  delete pe;
+  return KVQ_OK;
+}
+
+kvq_status kvq_peer_o_local(const kvq_peer* pe, int64_t epoch, void** out) {
+  if (!pe || !out || epoch <= 0) return KVQ_EINVAL;
+  *out = pe->win[pe->rank] + pe->L.o[epoch & 1];
+  return KVQ_OK;
+}
+
+kvq_status kvq_peer_publish_amax(const kvq_peer* pe, const void* K, const void* V, int64_t epoch, void* dev_scratch,
+                                 void* stream) {
+  if (!pe || !K || !V || !dev_scratch || epoch <= 0 || epoch >= (int64_t(1) << 32)) return KVQ_EINVAL;
+  const int Ts = pe->T_c / pe->P;
+  uint8_t* sc = static_cast<uint8_t*>(dev_scratch);
+  float* amax = reinterpret_cast<float*>(sc + kvq_ulysses_shard_scratch_bytes(Ts, pe->H));
+  kvq_status st = kvq_ulysses_shard_amax(K, V, pe->q_dtype, Ts, pe->H, pe->d, pe->k_smoothing, amax, dev_scratch, stream);
+  if (st != KVQ_OK) return st;
+  PeerPublishParams pp{};
+  pp.amax = amax;
+  pp.epoch = (unsigned long long)epoch;
+  pp.P = pe->P;
+  for (int r = 0; r < pe->P; ++r)
+    pp.mailbox[r] = reinterpret_cast<unsigned long long*>(pe->win[r] + pe->L.mailbox) + 2 * pe->rank;
+  return cuda_status(launch_peer_publish(pp, S(stream)));
+}
+
+kvq_status kvq_peer_pack(const kvq_peer* pe, const void* Q, const void* K, const void* V, int64_t epoch, void* stream) {
+  if (!pe || !Q || !K || !V || epoch <= 0 || epoch >= (int64_t(1) << 32)) return KVQ_EINVAL;
+  PackNvfp4Params p{};
+  p.x[0] = Q;
+  p.x[1] = K;
+  p.x[2] = V;
+  p.dtype = pe->q_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.Ts = pe->T_c / pe->P;
+  p.H = pe->H;
+  p.d = pe->d;
+  p.P = pe->P;
+  p.mode = (pe->scale_mode == 1 ? kModeSearch : 0) | (pe->k_smoothing ? kModeSmoothK : 0);
+  ulysses_partition(pe->H, pe->P, p.h0, p.owner);
+  for (int r = 0; r < pe->P; ++r) {
+    p.lay[r] = nvfp4_seg_layout(p.Ts, p.h0[r + 1] - p.h0[r], pe->d, (int)esize(pe->q_dtype), pe->k_smoothing != 0);
+    p.dst[r] = pe->win[r] + pe->L.recv + (int64_t)pe->rank * pe->L.seg;
+    p.arrive[r] = reinterpret_cast<unsigned long long*>(pe->win[r] + pe->L.arrive) + pe->rank;
+  }
+  p.mailbox = reinterpret_cast<const unsigned long long*>(pe->win[pe->rank] + pe->L.mailbox);
+  p.epoch = (unsigned long long)epoch;
+  return cuda_status(launch_ulysses_pack_nvfp4(p, S(stream)));
+}
+
+kvq_status kv_append_peer(const kvq_peer* pe, kvq_cache* c, int32_t layer, int64_t chunk_index, int64_t epoch,
+                          void* Q_out, void* stream) {
+  if (!pe || !c || !Q_out || epoch <= 0) return KVQ_EINVAL;
+  if (layer < 0 || layer >= c->cfg.num_layers || chunk_index < 0) return KVQ_EINVAL;
+  int32_t h0, h1;
+  kvq_head_partition(pe->H, pe->P, pe->rank, &h0, &h1);
+  if (c->cfg.num_heads != h1 - h0 || c->cfg.head_dim != pe->d || c->L.T_c != pe->T_c ||
+      c->cfg.k_smoothing != pe->k_smoothing || c->cfg.scale_mode != pe->scale_mode)
+    return KVQ_ESHAPE;
+  int slot = -1;
+  const kvq_status ss = select_slot(c, layer, chunk_index, &slot);
+  if (ss != KVQ_OK) return ss;
+  const int Hr = c->cfg.num_heads, d = c->cfg.head_dim, Ts = (int)(c->L.T_c / pe->P);
+  uint8_t* w = pe->win[pe->rank];
+  ScatterNvfp4Params p{};
+  p.recv = w + pe->L.recv;
+  p.lay = nvfp4_seg_layout(Ts, Hr, d, (int)esize(pe->q_dtype), c->cfg.k_smoothing != 0);
+  p.seg = pe->L.seg;
+  p.Ts = Ts;
+  p.Hr = Hr;
+  p.d = d;
+  p.es = (int)esize(pe->q_dtype);
+  p.P = pe->P;
+  for (int t = 0; t < 2; ++t) {
+    p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
+    p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);
+  }
+  p.mean = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
+  p.head_stride_rows = c->L.rows_per_head;
+  p.Q = Q_out;
+  p.amax = nullptr;
+  p.g_out = g_base(c, layer) + slot * 2;
+  p.status = status_ptr(c);
+  p.arrive = reinterpret_cast<const unsigned long long*>(w + pe->L.arrive);
+  p.arrive_target = (unsigned long long)epoch * (unsigned long long)ulysses_pack_grid(Ts, pe->H, d);
+  p.mailbox = reinterpret_cast<const unsigned long long*>(w + pe->L.mailbox);
+  p.epoch = (unsigned long long)epoch;
+  if (launch_ulysses_scatter_nvfp4(p, S(stream)) != cudaSuccess) return KVQ_ECUDA;
+  commit_slot(c, layer, chunk_index, slot);
+  return KVQ_OK;
+}
+
+kvq_status kvq_peer_signal_o(const kvq_peer* pe, int64_t epoch, void* stream) {
+  if (!pe || epoch <= 0) return KVQ_EINVAL;
+  PeerSignalParams p{};
+  p.P = pe->P;
+  p.value = (unsigned long long)epoch;
+  for (int r = 0; r < pe->P; ++r) p.slot[r] = reinterpret_cast<unsigned long long*>(pe->win[r] + pe->L.flags) + pe->rank;
+  return cuda_status(launch_peer_signal(p, S(stream)));
+}
+
+kvq_status kvq_peer_pull_o(const kvq_peer* pe, int64_t epoch, void* O_shard, void* stream) {
+  if (!pe || !O_shard || epoch <= 0) return KVQ_EINVAL;
+  PeerPullParams p{};
+  p.flags = reinterpret_cast<const unsigned long long*>(pe->win[pe->rank] + pe->L.flags);
+  p.epoch = (unsigned long long)epoch;
+  for (int r = 0; r < pe->P; ++r) p.o_src[r] = pe->win[r] + pe->L.o[epoch & 1];
+  p.out = static_cast<uint8_t*>(O_shard);
+  ulysses_partition(pe->H, pe->P, p.h0, p.owner);
+  p.Ts = pe->T_c / pe->P;
+  p.H = pe->H;
+  p.d = pe->d;
+  p.es = 2;  // bf16 O
+  p.P = pe->P;
+  p.rank = pe->rank;
+  return cuda_status(launch_peer_pull_o(p, S(stream)));
+}
+
 kvq_status kvq_debug_force_two_pass(kvq_cache* c, int32_t on) {
   if (!c) return KVQ_EINVAL;
   c->two_pass_only = on != 0;

@@ -156,6 +156,14 @@ struct PackNvfp4Params {
   Nvfp4SegLayout lay[kMaxP];  // its layout
   int h0[kMaxP + 1];
   uint8_t owner[256];
+  // f4 (peer memory): with dst[0] set, destination r's segment is stored straight into rank r's
+  // exchange window (dst[r], a peer pointer over NVLink); the global amax is the max of this
+  // rank's mailbox (P epoch-tagged entries, polled), and every CTA bumps each destination's arrival
+  // counter for this source (arrive[r], peer pointer) once its stores are done.
+  uint8_t* dst[kMaxP];
+  const unsigned long long* mailbox;  // [P][2] (epoch << 32 | amax bits)
+  unsigned long long* arrive[kMaxP];
+  unsigned long long epoch;
 };
 struct ScatterNvfp4Params {
   const uint8_t* recv;       // P segments of equal size (this rank is every source's destination)
@@ -167,10 +175,40 @@ struct ScatterNvfp4Params {
   float* mean;               // K-smoothing row means of the slot (head 0) or null
   int64_t head_stride_rows;
   void* Q;                   // out: [P*Ts, Hr, d] (dtype)
-  const float* amax;         // [2] global amax -> g of the slot
+  const float* amax;         // [2] global amax -> g of the slot (or null: from the mailbox)
   float* g_out;
   DevStatus* status;
+  // f4: wait until every source's arrival counter reached `arrive_target` (its stores landed), and
+  // take the amax from the mailbox when amax is null
+  const unsigned long long* arrive;   // [P] this rank's counters, or null
+  unsigned long long arrive_target;
+  const unsigned long long* mailbox;  // [P][2]
+  unsigned long long epoch;
 };
+struct PeerSignalParams {
+  unsigned long long* slot[kMaxP];   // peer r's flag for this rank (peer pointers)
+  unsigned long long value;
+  int P;
+};
+struct PeerPullParams {
+  const unsigned long long* flags;   // [P] this rank's flags, wait until all == epoch
+  unsigned long long epoch;
+  const uint8_t* o_src[kMaxP];       // owner r's O_local [P*Ts, H_r, d] (peer pointers)
+  uint8_t* out;                      // this rank's O shard [Ts, H, d]
+  int h0[kMaxP + 1];
+  uint8_t owner[256];
+  int Ts, H, d, es, P, rank;
+};
+struct PeerPublishParams {
+  const float* amax;                 // [2] this rank's shard amax (device)
+  unsigned long long* mailbox[kMaxP]; // peer r's mailbox entry pair for this rank (peer pointers)
+  unsigned long long epoch;
+  int P;
+};
+cudaError_t launch_peer_publish(const PeerPublishParams& p, cudaStream_t st);
+cudaError_t launch_peer_signal(const PeerSignalParams& p, cudaStream_t st);
+cudaError_t launch_peer_pull_o(const PeerPullParams& p, cudaStream_t st);
+int ulysses_pack_grid(int Ts, int H, int d);
 cudaError_t launch_ulysses_shard_amax(const QuantParams& p, uint32_t* partials, float* amax_out, cudaStream_t st);
 cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st);
 cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st);

@@ -975,6 +975,25 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
   constexpr int es = DT == DT_BF16 ? 2 : 4;
   const int64_t nblk = (int64_t)p.Ts * p.H * kNB;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool peer = p.dst[0] != nullptr;
+  __shared__ float s_amax[2];
+  if (peer) {  // f4: the global amax = max over this rank's mailbox, once all P entries are this epoch's
+    if (threadIdx.x < 2) {
+      uint32_t m = 0;
+      for (int r = 0; r < p.P; ++r) {
+        unsigned long long a;
+        for (;;) {
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p.mailbox + 2 * r + threadIdx.x) : "memory");
+          if ((a >> 32) == (p.epoch & 0xFFFFFFFFull)) break;
+          __nanosleep(64);
+        }
+        m = max(m, (uint32_t)a & 0x7FFFFFFFu);
+      }
+      s_amax[threadIdx.x] = __uint_as_float(m);
+    }
+    __syncthreads();
+  }
+  auto seg_of = [&](int r) { return peer ? p.dst[r] : p.send + p.seg_off[r]; };
   // ---- Q rows, passed through (16-byte chunks)
   {
     constexpr int cpr = D * es / 16;
@@ -986,14 +1005,14 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
       const int r = p.owner[h];
       const int Hp = p.h0[r + 1] - p.h0[r];
       const uint4 v = __ldg(reinterpret_cast<const uint4*>((const uint8_t*)p.x[0] + row * D * es) + cc);
-      uint8_t* o = p.send + p.seg_off[r] + p.lay[r].q + ((int64_t)t * Hp + (h - p.h0[r])) * D * es;
+      uint8_t* o = seg_of(r) + p.lay[r].q + ((int64_t)t * Hp + (h - p.h0[r])) * D * es;
       reinterpret_cast<uint4*>(o)[cc] = v;
     }
   }
   // ---- K, V blocks -> codes + scale bytes (+ K row means) in the destination's segment
   for (int t = 0; t < 2; ++t) {
     const bool smooth_t = SMOOTH && t == 0;
-    const uint32_t abits = __float_as_uint(p.amax[t]) & 0x7FFFFFFFu;
+    const uint32_t abits = __float_as_uint(peer ? s_amax[t] : p.amax[t]) & 0x7FFFFFFFu;
     if (abits >= 0x7F800000u) continue;  // non-finite: the receiver reports it, bytes undefined
     const float amax = __uint_as_float(abits);
     const float g = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
@@ -1026,10 +1045,18 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
       const int r = p.owner[h];
       const int Hp = p.h0[r + 1] - p.h0[r];
       const int64_t orow = (int64_t)tt * Hp + (h - p.h0[r]);
-      uint8_t* seg = p.send + p.seg_off[r];
+      uint8_t* seg = seg_of(r);
       *reinterpret_cast<uint2*>(seg + (t ? p.lay[r].vc : p.lay[r].kc) + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
       seg[(t ? p.lay[r].vs : p.lay[r].ks) + orow * kNB + j] = (uint8_t)sb[0];
       if (smooth_t && j == 0) reinterpret_cast<float*>(seg + p.lay[r].km)[orow] = mean;
+    }
+  }
+  if (peer) {  // this CTA's stores are done: make them visible system-wide, then count the arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int r = 0; r < p.P; ++r)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(p.arrive[r]) : "memory");
     }
   }
 }
@@ -1334,8 +1361,10 @@ cudaError_t pack_nvfp4_mode(const PackNvfp4Params& p, int grid, cudaStream_t st)
   return cudaGetLastError();
 }
 
+int ulysses_pack_grid(int Ts, int H, int d) { return grid_for((int64_t)Ts * H * (d / 16), 256); }
+
 cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st) {
-  const int grid = grid_for((int64_t)p.Ts * p.H * (p.d / 16), 256);
+  const int grid = ulysses_pack_grid(p.Ts, p.H, p.d);
   if (p.dtype == DT_BF16) return p.d == 128 ? pack_nvfp4_mode<DT_BF16, 128>(p, grid, st) : pack_nvfp4_mode<DT_BF16, 64>(p, grid, st);
   return p.d == 128 ? pack_nvfp4_mode<DT_FP32, 128>(p, grid, st) : pack_nvfp4_mode<DT_FP32, 64>(p, grid, st);
 }

@@ -111,6 +111,19 @@ __global__ void __launch_bounds__(256) unpack_o_kernel(const __grid_constant__ U
 // (head-major rows h * head_stride_rows + src * Ts + t) and Q into [P*Ts, Hr, d]; g of the slot
 // from the all-reduced amax (the sender quantized with the same g).
 __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constant__ ScatterNvfp4Params p) {
+  if (p.arrive) {  // f4: every source's stores into this window have landed
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < p.P; ++s) {
+        unsigned long long a;
+        for (;;) {
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p.arrive + s) : "memory");
+          if (a >= p.arrive_target) break;
+          __nanosleep(64);
+        }
+      }
+    }
+    __syncthreads();
+  }
   const int64_t rows = (int64_t)p.Ts * p.Hr;      // per source
   const int qc = p.d * p.es / 16, cc = p.d / 2 / 16;  // 16-byte chunks per Q row, per code row
   const int64_t per_src = rows * (qc + 2 * cc);
@@ -145,13 +158,63 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < 2) {
-    const uint32_t abits = __float_as_uint(p.amax[threadIdx.x]) & 0x7FFFFFFFu;
+    uint32_t mb = 0;
+    if (!p.amax)  // f4: the mailbox (complete: the senders read it before storing)
+      for (int r = 0; r < p.P; ++r) mb = max(mb, (uint32_t)p.mailbox[2 * r + threadIdx.x] & 0x7FFFFFFFu);
+    const uint32_t abits = (p.amax ? __float_as_uint(p.amax[threadIdx.x]) : mb) & 0x7FFFFFFFu;
     if (abits >= 0x7F800000u) {
       atomicCAS(&p.status->code, 0, -6);
     } else {
       const float amax = __uint_as_float(abits);
       p.g_out[threadIdx.x] = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 2688.0f);
     }
+  }
+}
+
+// f4: this rank's shard amax, epoch-tagged, into its entry pair of every peer's mailbox
+__global__ void peer_publish_kernel(const __grid_constant__ PeerPublishParams p) {
+  const int r = threadIdx.x >> 1, t = threadIdx.x & 1;
+  if (r < p.P) {
+    const unsigned long long v = (p.epoch << 32) | (__float_as_uint(p.amax[t]) & 0x7FFFFFFFu);
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mailbox[r] + t), "l"(v) : "memory");
+  }
+}
+
+// f4: one thread stores `value` (an epoch) into every peer's flag for this rank, after making this
+// rank's prior work (stream-ordered kernels) visible system-wide
+__global__ void peer_signal_kernel(const __grid_constant__ PeerSignalParams p) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < p.P; ++r)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.slot[r]), "l"(p.value) : "memory");
+  }
+}
+
+// f4: once every owner has signalled this epoch (its attention wrote O_local), pull this rank's token
+// rows of every head from the owners' O_local over peer memory (L2-only loads)
+__global__ void __launch_bounds__(256) peer_pull_o_kernel(const __grid_constant__ PeerPullParams p) {
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < p.P; ++r) {
+      unsigned long long a;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p.flags + r) : "memory");
+        if (a == p.epoch) break;
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+  const int cpr = p.d * p.es / 16;
+  const int64_t total = (int64_t)p.Ts * p.H * cpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cpr;
+    const int c = (int)(i - row * cpr);
+    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+    const int r = p.owner[h];
+    const int Hp = p.h0[r + 1] - p.h0[r];
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.o_src[r] + (((int64_t)p.rank * p.Ts + t) * Hp + (h - p.h0[r])) *
+                                                                           p.d * p.es) + c);
+    reinterpret_cast<uint4*>(p.out + row * p.d * p.es)[c] = v;
   }
 }
 
@@ -171,6 +234,21 @@ void partition_impl(int H, int P, int* h0, uint8_t* owner) {
 }  // namespace
 
 void ulysses_partition(int H, int P, int* h0, uint8_t* owner) { partition_impl(H, P, h0, owner); }
+
+cudaError_t launch_peer_publish(const PeerPublishParams& p, cudaStream_t st) {
+  peer_publish_kernel<<<1, 2 * kMaxP, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(const PeerSignalParams& p, cudaStream_t st) {
+  peer_signal_kernel<<<1, 32, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_pull_o(const PeerPullParams& p, cudaStream_t st) {
+  peer_pull_o_kernel<<<grid_for((int64_t)p.Ts * p.H * (p.d * p.es / 16)), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st) {
   const int64_t work = (int64_t)p.P * p.Ts * p.Hr * (p.d * p.es / 16 + p.d / 16);

@@ -94,6 +94,16 @@ _SIGS = {
                                [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
     "kv_append_ulysses_nvfp4": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, ctypes.c_int32, _P, _P,
                                                ctypes.c_int, _P]),
+    "kvq_peer_window_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 4 + [ctypes.c_int, ctypes.c_int32]),
+    "kvq_peer_create": (ctypes.c_int, [ctypes.c_int32] * 5 + [ctypes.c_int, ctypes.c_int32, ctypes.c_int32,
+                                                               ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "kvq_peer_destroy": (ctypes.c_int, [_P]),
+    "kvq_peer_o_local": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.POINTER(_P)]),
+    "kvq_peer_publish_amax": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, _P, _P]),
+    "kvq_peer_pack": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int64, _P]),
+    "kv_append_peer": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _P, _P]),
+    "kvq_peer_signal_o": (ctypes.c_int, [_P, ctypes.c_int64, _P]),
+    "kvq_peer_pull_o": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P]),
     "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
     "kvq_debug_set_trace": (ctypes.c_int, [_P]),
     "kvq_debug_force_two_pass": (ctypes.c_int, [_P, ctypes.c_int32]),
@@ -368,6 +378,62 @@ def ulysses_pack_nvfp4(Q, K, V, P, amax_kv, scale_search=False, k_smoothing=Fals
     return send, sizes
 
 
+def peer_window_bytes(T_c, H, d, P, q_dtype=torch.bfloat16, k_smoothing=False):
+    return int(lib().kvq_peer_window_bytes(T_c, H, d, P, _out_code(q_dtype), int(k_smoothing)))
+
+
+class PeerExchange:
+    """§8(f) f4: the NVFP4 exchange as device-initiated stores/loads over peer memory (include/kvq.h).
+    `window_ptrs`: the P ranks' window base addresses as seen from this rank (ints)."""
+
+    def __init__(self, T_c, H, d, P, rank, window_ptrs, q_dtype=torch.bfloat16, scale_search=False,
+                 k_smoothing=False, device="cuda"):
+        self.T_c, self.H, self.d, self.P, self.rank = T_c, H, d, P, rank
+        self.Ts = T_c // P
+        self.h0, self.h1 = head_partition(H, P, rank)
+        arr = (_P * P)(*[ctypes.c_void_p(int(w)) for w in window_ptrs])
+        self._arr = arr
+        h = _P()
+        _check(lib().kvq_peer_create(T_c, H, d, P, rank, _out_code(q_dtype), int(bool(scale_search)),
+                                     int(bool(k_smoothing)), arr, ctypes.byref(h)), "kvq_peer_create")
+        self._h = h
+        self.q_dtype = q_dtype
+        self.scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(self.Ts, H)) + 16, dtype=torch.uint8,
+                                   device=device)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().kvq_peer_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def o_local(self, epoch):
+        ptr = _P()
+        _check(lib().kvq_peer_o_local(self._h, epoch, ctypes.byref(ptr)), "kvq_peer_o_local")
+        return ptr.value
+
+    def publish_amax(self, K, V, epoch):
+        _check(lib().kvq_peer_publish_amax(self._h, _ptr(K), _ptr(V), epoch, _ptr(self.scratch), _stream()),
+               "kvq_peer_publish_amax")
+
+    def pack(self, Q, K, V, epoch):
+        _check(lib().kvq_peer_pack(self._h, _ptr(Q), _ptr(K), _ptr(V), epoch, _stream()), "kvq_peer_pack")
+
+    def append(self, cache, layer, chunk_index, epoch, Q_out):
+        _check(lib().kv_append_peer(self._h, cache._h, layer, chunk_index, epoch, _ptr(Q_out), _stream()),
+               "kv_append_peer")
+        return Q_out
+
+    def signal_o(self, epoch):
+        _check(lib().kvq_peer_signal_o(self._h, epoch, _stream()), "kvq_peer_signal_o")
+
+    def pull_o(self, epoch, out):
+        _check(lib().kvq_peer_pull_o(self._h, epoch, _ptr(out), _stream()), "kvq_peer_pull_o")
+        return out
+
+
 class Ulysses:
     """Head-sharded chunk step of one rank (App. C; App. D).
 
@@ -376,9 +442,12 @@ class Ulysses:
     of O (NCCL) -> head interleave (kernel).
     """
 
-    def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16, nvfp4_kv=False):
+    def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16, nvfp4_kv=False,
+                 peer=False):
         """nvfp4_kv (§8(f) f3): ship K/V as NVFP4 bytes quantized on the sender with
-        the all-reduced global amax (one extra tiny NCCL all-reduce; ~3.6x less K/V volume)."""
+        the all-reduced global amax (one extra tiny NCCL all-reduce; ~3.6x less K/V volume).
+        peer (§8(f) f4): the same payload moved by the kernels themselves over NVLink peer memory
+        (torch symmetric memory windows; no NCCL on the data path)."""
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.cache, self.H, self.d, self.T_c = cache, H, d, T_c
@@ -407,6 +476,21 @@ class Ulysses:
                              for p in range(world)]
         self.o_recv = torch.empty(sum(self.o_recv_sizes), dtype=torch.uint8, device=dev)
         self.es = es
+        self.peer = None
+        if peer:
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = group if group is not None else dist.group.WORLD
+            wb = peer_window_bytes(T_c, H, d, world, dtype, cache.k_smoothing)
+            self.win = symm_mem.empty(wb, dtype=torch.uint8, device=dev)
+            self.win.zero_()
+            if not symm_mem.is_symm_mem_enabled_for_group(grp.group_name):
+                symm_mem.enable_symm_mem_for_group(grp.group_name)
+            hdl = symm_mem.rendezvous(self.win, grp)
+            self.peer = PeerExchange(T_c, H, d, world, rank, list(hdl.buffer_ptrs), dtype, cache.scale_search,
+                                     cache.k_smoothing, device=dev)
+            self.epoch = 0
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=grp)
         # K-smoothing needs the amax of K_bar, which the bf16 exchange's piggybacked shard amax is not
         self.nvfp4_kv = bool(nvfp4_kv) or cache.k_smoothing
         if self.nvfp4_kv:
@@ -422,6 +506,20 @@ class Ulysses:
         """One layer of one chunk: Q, K, V are this rank's sequence shards [T_c/P, H, d]."""
         L, st = lib(), _stream()
         dt = _dt(Q)
+        if self.peer is not None:  # f4: publish amax -> pack into peers' windows -> append -> attention -> pull O
+            self.epoch += 1
+            ep, pe = self.epoch, self.peer
+            pe.publish_amax(K, V, ep)
+            pe.pack(Q, K, V, ep)
+            pe.append(self.cache, layer, chunk_index, ep, self.Q)
+            off = pe.o_local(ep) - self.win.data_ptr()
+            n = self.T_c * self.Hr * self.d * 2
+            O_loc = self.win[off:off + n].view(torch.bfloat16).view(self.T_c, self.Hr, self.d)
+            self.cache.attention(layer, self.Q, mask, out=O_loc)
+            pe.signal_o(ep)
+            if out is None:
+                out = torch.empty((self.Ts, self.H, self.d), dtype=torch.bfloat16, device=Q.device)
+            return pe.pull_o(ep, out)
         if self.nvfp4_kv:
             c = self.cache
             ulysses_shard_amax(K, V, c.k_smoothing, out=self.amax, scratch=self.amax_scratch)

@@ -141,3 +141,63 @@ def test_ulysses_nvfp4_exchange_simulated_matches_single_gpu(P, H, search, smoot
         assert torch.allclose(O_full, O_ref, rtol=1e-3, atol=2e-4)
         check_fp32_out(O_full.cpu().numpy(), orc.attend(0, ch, q.f64, sink, window))
 
+
+
+@pytest.mark.parametrize("P,H,search,smooth", [(2, 12, False, False), (4, 12, False, False), (8, 12, False, False),
+                                               (3, 7, False, False), (4, 12, True, True)])
+def test_peer_exchange_simulated_matches_single_gpu(P, H, search, smooth):
+    # §8(f) f4: the exchange as device-initiated stores/loads into the ranks' windows (peer memory on a
+    # multi-GPU box; P windows on one GPU here).  Kernels of all ranks run in phase order on one stream,
+    # so every device-side wait is already satisfied when reached.
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d = 40, 3, 128
+    T = tpf * fc
+    Ts = T // P
+    sink, window = 3, 9
+    parts = [kvq.head_partition(H, P, r) for r in range(P)]
+    mk = dict(sink_frames=sink, window_frames=window, max_chunk_slots=8, device=DEV, scale_search=search,
+              k_smoothing=smooth)
+    caches = [kvq.KVCache(1, h1 - h0, d, tpf, fc, **mk) for h0, h1 in parts]
+    ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    orc = OracleKVCache(1, H, d, tpf, fc, scale_search=search, k_smoothing=smooth)
+    wb = kvq.peer_window_bytes(T, H, d, P, k_smoothing=smooth)
+    wins = [torch.zeros(wb, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    ptrs = [w.data_ptr() for w in wins]
+    pes = [kvq.PeerExchange(T, H, d, P, r, ptrs, scale_search=search, k_smoothing=smooth) for r in range(P)]
+    for ch in range(5):
+        ep = ch + 1
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch, variant="outlier" if ch % 2 else "iid")
+        Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+        mask = kvq.Mask(ch, sink, window)
+        ref.append(0, ch, K, V)
+        O_ref = ref.attention(0, Q, mask, torch.float32)
+        orc.append(0, ch, k.f64, v.f64)
+        shards = [tuple(x[r * Ts:(r + 1) * Ts].contiguous() for x in (Q, K, V)) for r in range(P)]
+        for r in range(P):
+            pes[r].publish_amax(shards[r][1], shards[r][2], ep)
+        for r in range(P):
+            pes[r].pack(*shards[r], ep)
+        for p, (h0, h1) in enumerate(parts):
+            Ql = torch.empty((T, h1 - h0, d), dtype=torch.bfloat16, device=DEV)
+            pes[p].append(caches[p], 0, ch, ep, Ql)
+            assert torch.equal(Ql, Q[:, h0:h1])
+            off = pes[p].o_local(ep) - wins[p].data_ptr()
+            O_loc = wins[p][off:off + T * (h1 - h0) * d * 2].view(torch.bfloat16).view(T, h1 - h0, d)
+            caches[p].attention(0, Ql, mask, out=O_loc)
+        for p in range(P):
+            pes[p].signal_o(ep)
+        O_full = torch.cat([pes[r].pull_o(ep, torch.empty((Ts, H, d), dtype=torch.bfloat16, device=DEV))
+                            for r in range(P)])
+        O_ref_b = ref.attention(0, Q, mask, torch.bfloat16)
+        ex = ref.export(0, ch)
+        for p, (h0, h1) in enumerate(parts):
+            e = caches[p].export(0, ch)
+            for name in ("codes_k", "scales_k", "codes_v", "scales_v"):
+                full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
+                assert torch.equal(e[name], full), (p, name)
+            assert torch.equal(e["g_k"], ex["g_k"]) and torch.equal(e["g_v"], ex["g_v"])
+        assert torch.allclose(O_full.float(), O_ref_b.float(), rtol=1e-2, atol=2e-3)
+        ref_o = orc.attend(0, ch, q.f64, sink, window)
+        err = (O_full.float().cpu().numpy() - ref_o)
+        assert np.abs(err).max() <= 2e-3 + np.abs(ref_o).max() * 2 ** -8
