@@ -201,3 +201,42 @@ def test_peer_exchange_simulated_matches_single_gpu(P, H, search, smooth):
         ref_o = orc.attend(0, ch, q.f64, sink, window)
         err = (O_full.float().cpu().numpy() - ref_o)
         assert np.abs(err).max() <= 2e-3 + np.abs(ref_o).max() * 2 ** -8
+
+
+@pytest.mark.parametrize("exchange", ["bf16", "nvfp4", "peer"])
+def test_ulysses_class_world1_nccl(exchange):
+    # The Ulysses orchestration bench.py runs at N > 1 (NCCL all-to-all / all-reduce, torch symmetric
+    # memory windows for the peer exchange), exercised end to end with a one-rank NCCL group: the step's
+    # O and the cache bytes must equal the plain single-GPU path's
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    import socket
+
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tpf, fc, d, H = 40, 3, 128, 12
+        T = tpf * fc
+        mk = dict(sink_frames=3, window_frames=9, max_chunk_slots=8, device=DEV)
+        c_ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+        c_uly = kvq.KVCache(1, H, d, tpf, fc, **mk)
+        uly = kvq.Ulysses(c_uly, H, d, T, 0, 1, nvfp4_kv=exchange == "nvfp4", peer=exchange == "peer")
+        for ch in range(4):
+            q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch)
+            Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+            mask = kvq.Mask(ch, 3, 9)
+            c_ref.append(0, ch, K, V)
+            O_ref = c_ref.attention(0, Q, mask)
+            O = uly.step(0, ch, Q, K, V, mask)
+            torch.cuda.synchronize()
+            assert torch.equal(O, O_ref), (exchange, ch)
+            a, b = c_ref.export(0, ch), c_uly.export(0, ch)
+            assert all(torch.equal(a[n], b[n]) for n in a), (exchange, ch)
+    finally:
+        dist.destroy_process_group()

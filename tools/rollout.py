@@ -2,8 +2,8 @@
 per-chunk append) and configs[3] (L240: 240 s rollout, NVFP4 vs bf16 KV footprint and throughput).
 
 Reported (CUDA events, device time):
-  * W30 chunk step t = 0..8: 30 x (kv_quantize_append + chunk_attention), layer-query-tokens/s,
-    append share of the step (PAPER.md:146's "below 2%" context).
+  * W30 chunk step t = 0..8: 30 x (kv_quantize_append + chunk_attention) back to back, layer-query-
+    tokens/s, append share of the step (PAPER.md:146's "below 2%" context).
   * L240: 320 chunks x 30 layers, extrapolated from the measured ramp (t < 7) and steady (t >= 7)
     chunk steps; NVFP4 resident footprint vs bf16.
   * one steady layer step three ways: fused NVFP4 attention (this library), the paper's unfused
@@ -42,20 +42,20 @@ def main():
     steps = []
     for t in range(9):
         m = kvq.Mask(t, SINK, WIN)
-        ta = tq = 0.0
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        tot = 0.0
-        app = 0.0
+        # the 30 layers run back to back (no host sync inside the chunk step, as a rollout runs them);
+        # per-layer events on the stream then measure device time, the GPU never waits for the host
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)]
+        torch.cuda.synchronize()
         for layer in range(L):
             q, k, v = pool[(layer * 7 + t) % 4]
-            e[0].record()
+            ev[layer][0].record()
             cache.append(layer, t, k, v)
-            e[1].record()
+            ev[layer][1].record()
             cache.attention(layer, q, m, out=O)
-            e[2].record()
-            torch.cuda.synchronize()
-            app += e[0].elapsed_time(e[1])
-            tot += e[0].elapsed_time(e[2])
+            ev[layer][2].record()
+        torch.cuda.synchronize()
+        app = sum(ev[layer][0].elapsed_time(ev[layer][1]) for layer in range(L))
+        tot = ev[0][0].elapsed_time(ev[L - 1][2])
         steps.append({"chunk": t, "n_keys": cache.n_keys(0, m), "ms": tot, "append_ms": app,
                       "layer_query_tokens_per_s": L * T / (tot * 1e-3)})
     steady = steps[-1]["ms"]
