@@ -679,6 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 // pieces in increasing CTA order (deterministic).  A unit is split exactly when a CTA range boundary
 // falls strictly inside it; CTA b of this kernel handles the boundary of attention CTA b (if it is
 // the first boundary inside its unit), so only split units are touched.  Thread = (row, 4 columns).
+constexpr int kCombineSplit = 4;  // CTAs per split unit (row quarters): the merge is bandwidth per SM bound
+
 template <int D>
 __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ AttnParams p, int n) {
   const int64_t W = (int64_t)p.units * n;
@@ -695,8 +697,9 @@ __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ At
   while (c1 + 1 < G && range_begin(c1 + 1, W, G) < s1) ++c1;  // last CTA with a piece of the unit
   const int h = unit / p.qpairs, q0 = (unit - h * p.qpairs) * 256;
   constexpr int kTpr = D / 4;  // threads per row
-  for (int i = threadIdx.x; i < 256 * kTpr; i += blockDim.x) {
-    const int rr = i / kTpr, c4 = i - rr * kTpr;
+  constexpr int kRows = 256 / kCombineSplit;  // rows of the unit merged by this CTA (blockIdx.y)
+  for (int i = threadIdx.x; i < kRows * kTpr; i += blockDim.x) {
+    const int rr = blockIdx.y * kRows + i / kTpr, c4 = i % kTpr;
     const int t = q0 + rr;
     if (t >= p.Tq) continue;
     float m = -INFINITY;
@@ -751,7 +754,7 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   kern<<<G, kThreads, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess || !split) return e;
-  if (G > 1) combine_kernel<D><<<G - 1, 512, 0, st>>>(p, n);  // one CTA per range boundary
+  if (G > 1) combine_kernel<D><<<dim3(G - 1, kCombineSplit), 512, 0, st>>>(p, n);  // per range boundary
   return cudaGetLastError();
 }
 
