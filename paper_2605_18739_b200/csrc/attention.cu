@@ -679,7 +679,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 // pieces in increasing CTA order (deterministic).  A unit is split exactly when a CTA range boundary
 // falls strictly inside it; CTA b of this kernel handles the boundary of attention CTA b (if it is
 // the first boundary inside its unit), so only split units are touched.  Thread = (row, 4 columns).
-constexpr int kCombineSplit = 4;  // CTAs per split unit (row quarters): the merge is bandwidth per SM bound
+#ifndef KVQ_COMBINE_SPLIT
+#define KVQ_COMBINE_SPLIT 4
+#endif
+constexpr int kCombineSplit = KVQ_COMBINE_SPLIT;  // CTAs per split unit (row blocks): the merge is per-SM bandwidth bound
 
 template <int D>
 __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ AttnParams p, int n) {
