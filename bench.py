@@ -152,7 +152,8 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    force = args.force_ulysses and world == 1  # debug: the N>1 code path on one GPU (one-rank NCCL group)
+    if world > 1 or force:
         dist.init_process_group("nccl", device_id=dev)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -172,7 +173,7 @@ def run_gpu(args):
         chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
     dq = [tuple(x.to(dev) for x in c) for c in chunks]
     uly = (kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer")
-           if P > 1 else None)
+           if P > 1 or force else None)
 
     def step(c, out=None):
         q, k, v = dq[c]
@@ -371,6 +372,15 @@ def run_gpu(args):
         out["kv_stream_gbs"] = 2 * nk * H * D * 9 / 16 / (att_ms * 1e-3) / 1e9
         out["attention_tflops"] = ach
     else:
+        # per-phase breakdown of one distributed layer step (CUDA events per phase, median of 5 steps,
+        # max over ranks) -- SURVEY.md §8(d) D5
+        bd = uly.breakdown(lambda: step(CHUNK, O))
+        names = list(bd)
+        tb = torch.tensor([bd[n] for n in names], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        out["breakdown_ms"] = {n: float(v) for n, v in zip(names, tb.tolist())}
+        out["breakdown_ms"]["note"] = "per phase, median of 5 steps, max over ranks; exchange " + args.exchange
         # multi-GPU: the whole distributed layer step against the tensor roofline of all N GPUs
         ach = flops / (step_ms * 1e-3) / 1e12
         out["roofline"] = {"bound": "tensor", "kernel": "whole head-sharded layer step (pack, NCCL all-to-all, "
@@ -386,7 +396,7 @@ def run_gpu(args):
                                "sample": desc, "est_step_s": est}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if world > 1 or force:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -426,6 +436,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--force-ulysses", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "peer"],
                     help="N>1: bf16 all-to-all (NCCL), nvfp4 = §8(f) f3 (K/V quantized on the sender, NCCL), "
                          "peer = §8(f) f4 (the kernels store/load over NVLink peer memory, no NCCL on the data path)")

@@ -12,6 +12,7 @@ import math
 import os
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -476,6 +477,7 @@ class Ulysses:
                              for p in range(world)]
         self.o_recv = torch.empty(sum(self.o_recv_sizes), dtype=torch.uint8, device=dev)
         self.es = es
+        self.marks = None
         self.peer = None
         if peer:
             import torch.distributed._symmetric_memory as symm_mem
@@ -502,53 +504,92 @@ class Ulysses:
             self.amax_scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(self.Ts, H)), dtype=torch.uint8,
                                             device=dev)
 
+    def _mark(self, name):
+        """Phase boundary for the per-phase breakdown (CUDA event on the current stream) when
+        self.marks is a list; a no-op otherwise."""
+        if self.marks is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.marks.append((name, e))
+
     def step(self, layer, chunk_index, Q, K, V, mask: Mask, out=None):
         """One layer of one chunk: Q, K, V are this rank's sequence shards [T_c/P, H, d]."""
         L, st = lib(), _stream()
         dt = _dt(Q)
+        self._mark("start")
         if self.peer is not None:  # f4: publish amax -> pack into peers' windows -> append -> attention -> pull O
             self.epoch += 1
             ep, pe = self.epoch, self.peer
             pe.publish_amax(K, V, ep)
+            self._mark("amax_publish")
             pe.pack(Q, K, V, ep)
+            self._mark("quantize_pack_to_peers")
             pe.append(self.cache, layer, chunk_index, ep, self.Q)
+            self._mark("scatter_append")
             off = pe.o_local(ep) - self.win.data_ptr()
             n = self.T_c * self.Hr * self.d * 2
             O_loc = self.win[off:off + n].view(torch.bfloat16).view(self.T_c, self.Hr, self.d)
             self.cache.attention(layer, self.Q, mask, out=O_loc)
+            self._mark("attention")
             pe.signal_o(ep)
             if out is None:
                 out = torch.empty((self.Ts, self.H, self.d), dtype=torch.bfloat16, device=Q.device)
-            return pe.pull_o(ep, out)
+            pe.pull_o(ep, out)
+            self._mark("o_pull")
+            return out
         if self.nvfp4_kv:
             c = self.cache
             ulysses_shard_amax(K, V, c.k_smoothing, out=self.amax, scratch=self.amax_scratch)
+            self._mark("shard_amax")
             self.dist.all_reduce(self.amax, op=self.dist.ReduceOp.MAX, group=self.group)
+            self._mark("amax_allreduce")
             ulysses_pack_nvfp4(Q, K, V, self.P, self.amax, c.scale_search, c.k_smoothing, send=self.nv_send)
+            self._mark("quantize_pack")
             self.dist.all_to_all_single(self.nv_recv, self.nv_send, output_split_sizes=[self.nv_recv_seg] * self.P,
                                         input_split_sizes=self.nv_send_sizes, group=self.group)
+            self._mark("a2a_in")
             c.append_ulysses_nvfp4(layer, chunk_index, self.nv_recv, self.P, self.amax, Q_out=self.Q)
+            self._mark("scatter_append")
             return self._attend_and_return(layer, mask, out, Q)
         _check(L.kvq_ulysses_pack_qkv(_ptr(Q), _ptr(K), _ptr(V), dt, self.Ts, self.H, self.d, self.P,
                                       _ptr(self.send), _ptr(self.scratch), st), "kvq_ulysses_pack_qkv")
+        self._mark("pack")
         self.dist.all_to_all_single(self.recv, self.send, output_split_sizes=[self.recv_seg] * self.P,
                                     input_split_sizes=self.send_sizes, group=self.group)
+        self._mark("a2a_in")
         _check(L.kvq_ulysses_unpack_qkv(_ptr(self.recv), dt, self.Ts, self.Hr, self.d, self.P, _ptr(self.Q),
                                         _ptr(self.K), _ptr(self.V), _ptr(self.amax), st), "kvq_ulysses_unpack_qkv")
+        self._mark("unpack")
         self.cache.append(layer, chunk_index, self.K, self.V, amax_kv=self.amax)
+        self._mark("quantize_append")
         return self._attend_and_return(layer, mask, out, Q)
 
     def _attend_and_return(self, layer, mask, out, Q):
         L, st = lib(), _stream()
         self.cache.attention(layer, self.Q, mask, out=self.O_local)
+        self._mark("attention")
         o_send = self.O_local.view(torch.uint8).reshape(-1)
         self.dist.all_to_all_single(self.o_recv, o_send, output_split_sizes=self.o_recv_sizes,
                                     input_split_sizes=[o_send.numel() // self.P] * self.P, group=self.group)
+        self._mark("a2a_out")
         if out is None:
             out = torch.empty((self.Ts, self.H, self.d), dtype=torch.bfloat16, device=Q.device)
         _check(L.kvq_ulysses_unpack_o(_ptr(self.o_recv), KVQ_BF16, self.Ts, self.H, self.d, self.P, _ptr(out), st),
                "kvq_ulysses_unpack_o")
+        self._mark("unpack_o")
         return out
+
+    def breakdown(self, fn, reps=5):
+        """Median per-phase device time (ms) of `fn()` (one step), phases as marked in step()."""
+        rows = []
+        for _ in range(reps):
+            self.marks = []
+            fn()
+            torch.cuda.synchronize()
+            rows.append([(n, self.marks[i - 1][1].elapsed_time(e)) for i, (n, e) in enumerate(self.marks) if i])
+            self.marks = None
+        names = [n for n, _ in rows[0]]
+        return {n: float(np.median([r[i][1] for r in rows])) for i, n in enumerate(names)}
 
 
 def softmax_scale_default(d):
