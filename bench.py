@@ -172,7 +172,8 @@ def run_gpu(args):
         q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, ch)
         chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
     dq = [tuple(x.to(dev) for x in c) for c in chunks]
-    uly = (kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer")
+    uly = (kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer",
+                       nvfp4_q=args.exchange == "nvfp4q")
            if P > 1 or force else None)
 
     def step(c, out=None):
@@ -311,7 +312,7 @@ def run_gpu(args):
            # N>1 bf16 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted); nvfp4: amax (2-3),
            # reduce, pack, scatter, attention + combine, unpack O; peer: amax (2-3), reduce, publish, pack, scatter,
            # attention + combine, signal, pull
-           "gpu_launches": args.steps * (3 if world == 1 else {"bf16": 7, "nvfp4": 8, "peer": 10}[args.exchange])}
+           "gpu_launches": args.steps * (3 if world == 1 else {"bf16": 7, "nvfp4": 8, "nvfp4q": 11, "peer": 10}[args.exchange])}
     if uly is None:
         att_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_att]))
         app_ms_ev = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
@@ -437,8 +438,9 @@ def main():
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--force-ulysses", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "peer"],
+    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "nvfp4q", "peer"],
                     help="N>1: bf16 all-to-all (NCCL), nvfp4 = §8(f) f3 (K/V quantized on the sender, NCCL), "
+                         "nvfp4q = nvfp4 with Q cast to NVFP4 too (PAPER.md:646; a different numerics mode), "
                          "peer = §8(f) f4 (the kernels store/load over NVLink peer memory, no NCCL on the data path)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -229,26 +229,44 @@ kvq_status kvq_ulysses_shard_amax(const void* K, const void* V, kvq_dtype dtype,
                                   void* dev_scratch, void* stream);
 
 /* Bytes of the segment for destination `dst` (= bytes received from every source when dst is
- * this rank): per row (t, h_dst) Q d*esize(q_dtype), K and V codes d/2 + scales d/16 each (+ a
- * fp32 K mean with k_smoothing), each part padded to 16 bytes. */
+ * this rank): per row (t, h_dst) Q d*esize(q_dtype) (or, with q_nvfp4, d/2 code + d/16 scale
+ * bytes), K and V codes d/2 + scales d/16 each (+ a fp32 K mean with k_smoothing), each part
+ * padded to 16 bytes. */
 size_t kvq_ulysses_nvfp4_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst,
-                               kvq_dtype q_dtype, int32_t k_smoothing);
+                               kvq_dtype q_dtype, int32_t k_smoothing, int32_t q_nvfp4);
+
+/* max |Q| of this rank's shard (dev fp32[1]); scratch as for kvq_ulysses_shard_amax. */
+kvq_status kvq_ulysses_q_amax(const void* Q, kvq_dtype dtype, int32_t Ts, int32_t H, int32_t d,
+                              float* dev_amax_q, void* dev_scratch, void* stream);
 
 /* Quantize + pack this rank's shard (Q, K, V dev [Ts, H, d]) into the all-to-allv send buffer,
  * destination segments in rank order.  dev_amax_kv: the GLOBAL amax (all-reduced) -> g =
- * RN32(amax/2688); scale_mode / k_smoothing must match the receiving caches' config. */
+ * RN32(amax/2688); scale_mode / k_smoothing must match the receiving caches' config.
+ * dev_amax_q: null = Q travels in its dtype; else the GLOBAL amax of Q and Q is cast to NVFP4 too
+ * ("we also cast the runtime Q to NVFP4 immediately before the pre-attention
+ * All-to-All"; plain R1 encoding) -- a different attention numerics mode (reading Z24). */
 kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, kvq_dtype dtype,
                                   int32_t Ts, int32_t H, int32_t d, int32_t P,
-                                  const float* dev_amax_kv, int32_t scale_mode,
-                                  int32_t k_smoothing, void* send_buf, void* stream);
+                                  const float* dev_amax_kv, const float* dev_amax_q,
+                                  int32_t scale_mode, int32_t k_smoothing, void* send_buf,
+                                  void* stream);
 
 /* Receiving side: the P received segments (this rank's H_r = cache num_heads heads, Ts = T_c/P
  * tokens each) become chunk `chunk_index` of `layer` under the append policy of
  * kv_quantize_append (same slot / eviction rules, same error codes), g of the slot from
- * dev_amax_kv, and Q_out dev [T_c, H_r, d] (q_dtype) receives the chunk's queries. */
+ * dev_amax_kv, and Q_out dev [T_c, H_r, d] receives the chunk's queries: in q_dtype, or, with
+ * dev_amax_q (NVFP4 Q; dev_q_scale must then be given too), as fp16 dec(c) dec(s) -- exact --
+ * with *dev_q_scale = g_Q; attend with chunk_attention_qscaled. */
 kvq_status kv_append_ulysses_nvfp4(kvq_cache* cache, int32_t layer, int64_t chunk_index,
                                    const void* recv_buf, int32_t P, const float* dev_amax_kv,
-                                   void* Q_out, kvq_dtype q_dtype, void* stream);
+                                   const float* dev_amax_q, void* Q_out, kvq_dtype q_dtype,
+                                   float* dev_q_scale, void* stream);
+
+/* chunk_attention for NVFP4-exchanged queries: Q dev [T_c, H, d] fp16 holding dec(c) dec(s),
+ * scores scaled by g_Q = *dev_q_scale (device fp32) on top of softmax_scale. */
+kvq_status chunk_attention_qscaled(kvq_cache* cache, int32_t layer, const void* Q_fp16,
+                                   const float* dev_q_scale, const kvq_mask* mask,
+                                   float softmax_scale, void* O, kvq_dtype out_dtype, void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Device-initiated exchange over peer memory (§8(f) f4): the NVFP4 exchange above without NCCL.

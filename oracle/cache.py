@@ -65,7 +65,14 @@ class OracleKVCache:
         return np.concatenate(Ks), np.concatenate(Vs)
 
     def attend(self, layer, chunk_index, Q, sink_frames, window_frames, shot_start=0, shot_len=0,
-               softmax_scale=None, rows=None):
-        """chunk_attention: softmax(Q K^T/sqrt(d)) V over K_eff(t)."""
+               softmax_scale=None, rows=None, q_nvfp4=False):
+        """chunk_attention: softmax(Q K^T/sqrt(d)) V over K_eff(t).
+        q_nvfp4: the queries are NVFP4-quantized first, as one (T_c H) x d tensor with the plain
+        encoding ("cast the runtime Q to NVFP4" before the all-to-all; reading Z24),
+        and attention uses the exact dequantized Q^ = dec(c) dec(s) g_Q."""
         K, V = self.keys(layer, chunk_index, sink_frames, window_frames, shot_start, shot_len)
+        if q_nvfp4:
+            Q = np.asarray(Q, dtype=np.float64)
+            T, H, d = Q.shape
+            Q = nvfp4.dequantize_kv_chunk(nvfp4.quantize_kv_chunk(Q), T, H, d)
         return attention(Q, K, V, softmax_scale, rows)

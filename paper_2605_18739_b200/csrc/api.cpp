@@ -346,12 +346,27 @@ kvq_status kv_quantize_append_amax(kvq_cache* c, int32_t layer, int64_t chunk, c
   return append_impl(c, layer, chunk, K, V, dt, dev_amax_kv, stream);
 }
 
+static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
+                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream);
+
 kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
                            float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  return attention_impl(c, layer, Q, q_dtype, nullptr, mask, softmax_scale, O, out_dtype, stream);
+}
+
+kvq_status chunk_attention_qscaled(kvq_cache* c, int32_t layer, const void* Q_fp16, const float* dev_q_scale,
+                                   const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype,
+                                   void* stream) {
+  if (!dev_q_scale) return KVQ_EINVAL;
+  return attention_impl(c, layer, Q_fp16, KVQ_FP16, dev_q_scale, mask, softmax_scale, O, out_dtype, stream);
+}
+
+static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
+                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
   if (!c || !Q || !O || !mask) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || mask->chunk_index < 0) return KVQ_EINVAL;
   if (mask->sink_frames < 0 || mask->window_frames < 0 || mask->shot_len_frames < 0) return KVQ_EINVAL;
-  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
   if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
   AttnParams p{};
   std::vector<AttnSeg> segs;
@@ -361,7 +376,8 @@ kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype
   std::copy(segs.begin(), segs.end(), p.seg);
   const int d = c->cfg.head_dim;
   p.Q = Q;
-  p.q_dtype = q_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.q_dtype = q_dtype == KVQ_BF16 ? DT_BF16 : (q_dtype == KVQ_FP16 ? DT_FP16 : DT_FP32);
+  p.q_scale = q_scale;
   p.O = O;
   p.out_dtype = out_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
   p.mean_k = mean_base(c, layer);
@@ -602,10 +618,31 @@ size_t kvq_ulysses_shard_scratch_bytes(int32_t Ts, int32_t H) {
 }
 
 size_t kvq_ulysses_nvfp4_bytes(int32_t Ts, int32_t H, int32_t d, int32_t P, int32_t dst, kvq_dtype q_dtype,
-                               int32_t k_smoothing) {
+                               int32_t k_smoothing, int32_t q_nvfp4) {
   int32_t h0, h1;
   kvq_head_partition(H, P, dst, &h0, &h1);
-  return (size_t)nvfp4_seg_layout(Ts, h1 - h0, d, (int)esize(q_dtype), k_smoothing != 0).total;
+  return (size_t)nvfp4_seg_layout(Ts, h1 - h0, d, (int)esize(q_dtype), k_smoothing != 0, q_nvfp4 != 0).total;
+}
+
+kvq_status kvq_ulysses_q_amax(const void* Q, kvq_dtype dtype, int32_t Ts, int32_t H, int32_t d, float* dev_amax_q,
+                              void* dev_scratch, void* stream) {
+  if (!Q || !dev_amax_q || !dev_scratch || Ts <= 0 || H <= 0) return KVQ_EINVAL;
+  if (d != 64 && d != 128) return KVQ_ESHAPE;
+  if (dtype != KVQ_BF16 && dtype != KVQ_FP32) return KVQ_EDTYPE;
+  // amax kernels over (Q, Q): both reduced values are amax(Q); the first is kept
+  uint8_t* sc = static_cast<uint8_t*>(dev_scratch);
+  QuantParams p{};
+  p.x[0] = Q;
+  p.x[1] = Q;
+  p.dtype = dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.rows = Ts * H;
+  p.H = H;
+  p.d = d;
+  p.status = reinterpret_cast<DevStatus*>(sc + 2 * kNumPartials * sizeof(uint32_t));
+  float* two = reinterpret_cast<float*>(sc + 2 * kNumPartials * sizeof(uint32_t) + 32);
+  cudaError_t e = launch_ulysses_shard_amax(p, reinterpret_cast<uint32_t*>(sc), two, S(stream));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dev_amax_q, two, sizeof(float), cudaMemcpyDeviceToDevice, S(stream));
+  return cuda_status(e);
 }
 
 kvq_status kvq_ulysses_shard_amax(const void* K, const void* V, kvq_dtype dtype, int32_t Ts, int32_t H, int32_t d,
@@ -633,8 +670,8 @@ kvq_status kvq_ulysses_shard_amax(const void* K, const void* V, kvq_dtype dtype,
 }
 
 kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, kvq_dtype dtype, int32_t Ts, int32_t H,
-                                  int32_t d, int32_t P, const float* dev_amax_kv, int32_t scale_mode,
-                                  int32_t k_smoothing, void* send_buf, void* stream) {
+                                  int32_t d, int32_t P, const float* dev_amax_kv, const float* dev_amax_q,
+                                  int32_t scale_mode, int32_t k_smoothing, void* send_buf, void* stream) {
   if (!Q || !K || !V || !dev_amax_kv || !send_buf || Ts <= 0 || H <= 0 || H > 256 || P <= 0 || P > kMaxP)
     return KVQ_EINVAL;
   if (d != 64 && d != 128) return KVQ_ESHAPE;
@@ -651,22 +688,25 @@ kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, k
   p.P = P;
   p.mode = (scale_mode == 1 ? kModeSearch : 0) | (k_smoothing ? kModeSmoothK : 0);
   p.amax = dev_amax_kv;
+  p.amax_q = dev_amax_q;
   p.send = static_cast<uint8_t*>(send_buf);
   ulysses_partition(H, P, p.h0, p.owner);
   int64_t off = 0;
   for (int r = 0; r < P; ++r) {
     p.seg_off[r] = off;
-    p.lay[r] = nvfp4_seg_layout(Ts, p.h0[r + 1] - p.h0[r], d, (int)esize(dtype), k_smoothing != 0);
+    p.lay[r] = nvfp4_seg_layout(Ts, p.h0[r + 1] - p.h0[r], d, (int)esize(dtype), k_smoothing != 0, dev_amax_q != nullptr);
     off += p.lay[r].total;
   }
   return cuda_status(launch_ulysses_pack_nvfp4(p, S(stream)));
 }
 
 kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_index, const void* recv_buf, int32_t P,
-                                   const float* dev_amax_kv, void* Q_out, kvq_dtype q_dtype, void* stream) {
+                                   const float* dev_amax_kv, const float* dev_amax_q, void* Q_out, kvq_dtype q_dtype,
+                                   float* dev_q_scale, void* stream) {
   if (!c || !recv_buf || !dev_amax_kv || !Q_out || P <= 0 || P > kMaxP) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || chunk_index < 0) return KVQ_EINVAL;
   if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if ((dev_amax_q == nullptr) != (dev_q_scale == nullptr)) return KVQ_EINVAL;
   if (c->L.T_c % P) return KVQ_ESHAPE;
   int slot = -1;
   const kvq_status ss = select_slot(c, layer, chunk_index, &slot);
@@ -674,13 +714,16 @@ kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_in
   const int Hr = c->cfg.num_heads, d = c->cfg.head_dim, Ts = (int)(c->L.T_c / P);
   ScatterNvfp4Params p{};
   p.recv = static_cast<const uint8_t*>(recv_buf);
-  p.lay = nvfp4_seg_layout(Ts, Hr, d, (int)esize(q_dtype), c->cfg.k_smoothing != 0);
+  const bool qn = dev_amax_q != nullptr;
+  p.lay = nvfp4_seg_layout(Ts, Hr, d, (int)esize(q_dtype), c->cfg.k_smoothing != 0, qn);
   p.seg = p.lay.total;
   p.Ts = Ts;
   p.Hr = Hr;
   p.d = d;
-  p.es = (int)esize(q_dtype);
+  p.es = qn ? 2 : (int)esize(q_dtype);  // NVFP4 Q arrives as fp16 dec(c) dec(s)
   p.P = P;
+  p.amax_q = dev_amax_q;
+  p.q_scale_out = dev_q_scale;
   for (int t = 0; t < 2; ++t) {
     p.codes[t] = codes_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 2);
     p.scales[t] = scales_base(c, t, layer) + (size_t)slot * c->L.T_pad * (d / 16);

@@ -158,7 +158,10 @@ KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, 
     uint32_t o[4] = {0, 0, 0, 0}, ol[4] = {0, 0, 0, 0};
     if (valid) {
       float f[8];
-      if (!QSPLIT && q_dtype == DT_BF16) {
+      if (!QSPLIT && q_dtype == DT_FP16) {  // NVFP4-exchanged Q: fp16 dec(c) dec(s), copied as is
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>((const __half*)Q + row_index * D) + c);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+      } else if (!QSPLIT && q_dtype == DT_BF16) {
         uint4 v = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)Q + row_index * D) + c);
         if (MMA_BF16) {
           o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
@@ -333,13 +336,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     const uint32_t tS = tmem + 128 * qi + lane_off;
     const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
     int g = 0;  // global tile counter (barrier parity)
+    // exponent scale (log2 units); NVFP4-exchanged Q carries g_Q (device scalar) into it
+    const float sl2 = p.q_scale ? p.scale_log2 * __ldg(p.q_scale) : p.scale_log2;
     Piece pc;
     for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
       const float qsum = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
                                                                  (int64_t)t * H + h, t < p.Tq);
-      const uint64_t qsb2 = f32x2_pack(qsum * p.scale_log2, qsum * p.scale_log2);
+      const uint64_t qsb2 = f32x2_pack(qsum * sl2, qsum * sl2);
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
       float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           gk = __ldg(p.g + 2 * sg.slot);
           gv = __ldg(p.g + 2 * sg.slot + 1);
         }
-        const float cs = gk * p.scale_log2;
+        const float cs = gk * sl2;
         float mean_r = 0.0f;  // SMOOTH: this thread's key of the tile
         if (SMOOTH && row >= lo && row < hi)
           mean_r = __ldg(p.mean_k + (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + row);

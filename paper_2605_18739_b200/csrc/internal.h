@@ -89,6 +89,7 @@ struct AttnParams {
   const void* Vb;
   int Tq, H, d;
   float scale_log2;          // softmax_scale * log2(e)
+  const float* q_scale;      // NVFP4 Q exchange: Q holds fp16 dec(c) dec(s), scores x g_Q = *q_scale (or null)
   // persistent stream-K schedule (filled by launch_attention)
   unsigned long long* trace; // debug timeline of CTA 0 (null in production)
   float* ws;                 // partial-piece workspace (null: one CTA per unit, no partials)
@@ -132,14 +133,17 @@ cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int 
 // smoothing], every part padded to 16 bytes.
 constexpr int kMaxP = 64;
 struct Nvfp4SegLayout {
-  int64_t q, kc, ks, vc, vs, km, total;  // byte offsets within the segment, total size
+  int64_t q, qs, kc, ks, vc, vs, km, total;  // byte offsets within the segment, total size
 };
 inline int64_t pad16(int64_t x) { return (x + 15) & ~int64_t(15); }
-inline Nvfp4SegLayout nvfp4_seg_layout(int Ts, int Hp, int d, int es, bool smooth) {
+// q_nvfp4: Q travels as NVFP4 too (codes at q, scale bytes at qs; "cast the runtime Q
+// to NVFP4"), else as rows of d * es bytes at q
+inline Nvfp4SegLayout nvfp4_seg_layout(int Ts, int Hp, int d, int es, bool smooth, bool q_nvfp4 = false) {
   Nvfp4SegLayout L{};
   const int64_t rows = (int64_t)Ts * Hp;
   L.q = 0;
-  L.kc = pad16(rows * d * es);
+  L.qs = q_nvfp4 ? pad16(rows * d / 2) : pad16(rows * d * es);
+  L.kc = q_nvfp4 ? L.qs + pad16(rows * d / 16) : L.qs;
   L.ks = L.kc + pad16(rows * d / 2);
   L.vc = L.ks + pad16(rows * d / 16);
   L.vs = L.vc + pad16(rows * d / 2);
@@ -151,6 +155,7 @@ struct PackNvfp4Params {
   const void* x[3];          // Q, K, V shards [Ts, H, d] (dtype)
   int dtype, Ts, H, d, P, mode;
   const float* amax;         // [2] global amax of K (K_bar with smoothing) and V over all ranks
+  const float* amax_q;       // global amax of Q: Q travels as NVFP4 (plain R1 encoding); null: as is
   uint8_t* send;
   int64_t seg_off[kMaxP];    // byte offset of destination r's segment
   Nvfp4SegLayout lay[kMaxP];  // its layout
@@ -176,6 +181,8 @@ struct ScatterNvfp4Params {
   int64_t head_stride_rows;
   void* Q;                   // out: [P*Ts, Hr, d] (dtype)
   const float* amax;         // [2] global amax -> g of the slot (or null: from the mailbox)
+  const float* amax_q;       // NVFP4 Q: its global amax; Q_out then holds fp16 dec(c) dec(s) (exact)
+  float* q_scale_out;        //   and *q_scale_out = g_Q = RN32(amax_q / 2688)
   float* g_out;
   DevStatus* status;
   // f4: wait until every source's arrival counter reached `arrive_target` (its stores landed), and

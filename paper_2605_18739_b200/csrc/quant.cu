@@ -994,8 +994,32 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
     __syncthreads();
   }
   auto seg_of = [&](int r) { return peer ? p.dst[r] : p.send + p.seg_off[r]; };
-  // ---- Q rows, passed through (16-byte chunks)
-  {
+  // ---- Q rows: NVFP4 (plain R1, the global amax_q) or passed through (16-byte chunks)
+  if (p.amax_q) {
+    const uint32_t qbits = __float_as_uint(p.amax_q[0]) & 0x7FFFFFFFu;
+    if (qbits < 0x7F800000u) {
+      const float qa = __uint_as_float(qbits);
+      const float g = qa == 0.0f ? 1.0f : __fdiv_rn(qa, 2688.0f);
+      const float rg = __frcp_rn(g);
+      const bool exact = !(g >= 0x1p-60f && g <= 0x1p60f);
+      for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nblk; u += stride) {
+        float v[1][16];
+        unpack_block16<DT>((const uint8_t*)p.x[0] + u * kUB, v[0]);
+        uint32_t sb[1], w0[1], w1[1];
+        const uint32_t flags = exact ? 1u : quantize_blocks_fast<1, false>(v, g, rg, sb, w0, w1);
+        if (flags) quantize_block16_exact<false>(v[0], g, sb[0], w0[0], w1[0]);
+        const int64_t row = u / kNB;
+        const int j = (int)(u - row * kNB);
+        const int tt = (int)(row / p.H), h = (int)(row - (int64_t)tt * p.H);
+        const int r = p.owner[h];
+        const int Hp = p.h0[r + 1] - p.h0[r];
+        const int64_t orow = (int64_t)tt * Hp + (h - p.h0[r]);
+        uint8_t* seg = seg_of(r);
+        *reinterpret_cast<uint2*>(seg + p.lay[r].q + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
+        seg[p.lay[r].qs + orow * kNB + j] = (uint8_t)sb[0];
+      }
+    }
+  } else {
     constexpr int cpr = D * es / 16;
     const int64_t total = (int64_t)p.Ts * p.H * cpr;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {

@@ -136,8 +136,16 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
       const int64_t row = r / qc;
       const int c = (int)(r - row * qc);
       const int t = (int)(row / p.Hr), h = (int)(row - (int64_t)t * p.Hr);
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + row * p.d * p.es) + c);
-      reinterpret_cast<uint4*>((uint8_t*)p.Q + (((int64_t)src * p.Ts + t) * p.Hr + h) * p.d * p.es)[c] = v;
+      uint8_t* qdst = (uint8_t*)p.Q + (((int64_t)src * p.Ts + t) * p.Hr + h) * p.d * p.es;
+      if (p.amax_q) {  // NVFP4 Q: 8 elements per 16-byte chunk of the fp16 row = dec(c) dec(s), exact
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(seg + p.lay.q + row * (p.d / 2) + c * 4);
+        const uint32_t sb = seg[p.lay.qs + row * (p.d / 16) + c / 2];
+        uint32_t o[4];
+        dequant_word_f16(w, f16x2_from_e4m3x2(sb | (sb << 8)), o);
+        reinterpret_cast<uint4*>(qdst)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+      } else {
+        reinterpret_cast<uint4*>(qdst)[c] = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + row * p.d * p.es) + c);
+      }
       continue;
     }
     r -= rows * qc;
@@ -156,6 +164,11 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
       else *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(sc);
       if (tsr == 0 && p.mean) p.mean[orow] = reinterpret_cast<const float*>(seg + p.lay.km)[row];
     }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 2 && p.amax_q) {  // g_Q for the attention's score scale
+    const uint32_t qb = __float_as_uint(p.amax_q[0]) & 0x7FFFFFFFu;
+    if (qb >= 0x7F800000u) atomicCAS(&p.status->code, 0, -6);
+    else *p.q_scale_out = qb == 0 ? 1.0f : __fdiv_rn(__uint_as_float(qb), 2688.0f);
   }
   if (blockIdx.x == 0 && threadIdx.x < 2) {
     uint32_t mb = 0;

@@ -88,13 +88,16 @@ _SIGS = {
     "kvq_ulysses_unpack_o": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, _P, _P]),
     "kvq_ulysses_shard_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
-    "kvq_ulysses_nvfp4_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 5 + [ctypes.c_int, ctypes.c_int32]),
+    "kvq_ulysses_nvfp4_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 5 + [ctypes.c_int, ctypes.c_int32, ctypes.c_int32]),
+    "kvq_ulysses_q_amax": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P]),
+    "chunk_attention_qscaled": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, ctypes.POINTER(_Mask), ctypes.c_float, _P,
+                                               ctypes.c_int, _P]),
     "kvq_ulysses_shard_amax": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                               ctypes.c_int32, _P, _P, _P]),
     "kvq_ulysses_pack_nvfp4": (ctypes.c_int, [_P, _P, _P, ctypes.c_int] + [ctypes.c_int32] * 4 +
-                               [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
-    "kv_append_ulysses_nvfp4": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, ctypes.c_int32, _P, _P,
-                                               ctypes.c_int, _P]),
+                               [_P, _P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
+    "kv_append_ulysses_nvfp4": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, ctypes.c_int32, _P, _P, _P,
+                                               ctypes.c_int, _P, _P]),
     "kvq_peer_window_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 4 + [ctypes.c_int, ctypes.c_int32]),
     "kvq_peer_create": (ctypes.c_int, [ctypes.c_int32] * 5 + [ctypes.c_int, ctypes.c_int32, ctypes.c_int32,
                                                                ctypes.POINTER(_P), ctypes.POINTER(_P)]),
@@ -227,13 +230,31 @@ class KVCache:
                                      _out_code(out.dtype), _stream()), "chunk_attention")
         return out
 
-    def append_ulysses_nvfp4(self, layer, chunk_index, recv, P, amax_kv, q_dtype=torch.bfloat16, Q_out=None):
-        """kv_append_ulysses_nvfp4: the P received NVFP4 segments become chunk `chunk_index`; returns Q."""
+    def append_ulysses_nvfp4(self, layer, chunk_index, recv, P, amax_kv, q_dtype=torch.bfloat16, Q_out=None,
+                             amax_q=None, q_scale=None):
+        """kv_append_ulysses_nvfp4: the P received NVFP4 segments become chunk `chunk_index`; returns Q
+        (with amax_q: fp16 dec(c) dec(s), and q_scale [1] receives g_Q)."""
         if Q_out is None:
-            Q_out = torch.empty((self.T_c, self.H, self.d), dtype=q_dtype, device=self.device)
-        _check(lib().kv_append_ulysses_nvfp4(self._h, layer, chunk_index, _ptr(recv), P, _ptr(amax_kv), _ptr(Q_out),
-                                             _out_code(Q_out.dtype), _stream()), "kv_append_ulysses_nvfp4")
-        return Q_out
+            Q_out = torch.empty((self.T_c, self.H, self.d), dtype=torch.float16 if amax_q is not None else q_dtype,
+                                device=self.device)
+        if amax_q is not None and q_scale is None:
+            q_scale = torch.empty(1, dtype=torch.float32, device=self.device)
+        qd = q_dtype if amax_q is not None else Q_out.dtype
+        _check(lib().kv_append_ulysses_nvfp4(self._h, layer, chunk_index, _ptr(recv), P, _ptr(amax_kv),
+                                             _ptr(amax_q) if amax_q is not None else None, _ptr(Q_out), _out_code(qd),
+                                             _ptr(q_scale) if q_scale is not None else None, _stream()),
+               "kv_append_ulysses_nvfp4")
+        return (Q_out, q_scale) if amax_q is not None else Q_out
+
+    def attention_qscaled(self, layer, Q16, q_scale, mask: Mask, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None):
+        """chunk_attention_qscaled: attention for NVFP4-exchanged queries (fp16 dec(c) dec(s), scale g_Q)."""
+        self._shape_ok(Q16)
+        if out is None:
+            out = torch.empty(Q16.shape, dtype=out_dtype, device=Q16.device)
+        m = mask._c()
+        _check(lib().chunk_attention_qscaled(self._h, layer, _ptr(Q16), _ptr(q_scale), ctypes.byref(m), softmax_scale,
+                                             _ptr(out), _out_code(out.dtype), _stream()), "chunk_attention_qscaled")
+        return out
 
     def dequantize(self, layer, chunk_index, out_dtype=torch.float32):
         K = torch.empty((self.T_c, self.H, self.d), dtype=out_dtype, device=self.device)
@@ -351,8 +372,20 @@ def ulysses_unpack_o(recv, Ts, H, d, P, dtype=torch.bfloat16, out=None):
     return out
 
 
-def ulysses_nvfp4_bytes(Ts, H, d, P, dst, q_dtype=torch.bfloat16, k_smoothing=False):
-    return int(lib().kvq_ulysses_nvfp4_bytes(Ts, H, d, P, dst, _out_code(q_dtype), int(k_smoothing)))
+def ulysses_nvfp4_bytes(Ts, H, d, P, dst, q_dtype=torch.bfloat16, k_smoothing=False, q_nvfp4=False):
+    return int(lib().kvq_ulysses_nvfp4_bytes(Ts, H, d, P, dst, _out_code(q_dtype), int(k_smoothing), int(q_nvfp4)))
+
+
+def ulysses_q_amax(Q, out=None, scratch=None):
+    """kvq_ulysses_q_amax: max |Q| of this rank's shard (dev fp32[1])."""
+    Ts, H, d = Q.shape
+    if out is None:
+        out = torch.empty(1, dtype=torch.float32, device=Q.device)
+    if scratch is None:
+        scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(Ts, H)), dtype=torch.uint8, device=Q.device)
+    _check(lib().kvq_ulysses_q_amax(_ptr(Q), _dt(Q), Ts, H, d, _ptr(out), _ptr(scratch), _stream()),
+           "kvq_ulysses_q_amax")
+    return out
 
 
 def ulysses_shard_amax(K, V, k_smoothing=False, out=None, scratch=None):
@@ -367,15 +400,16 @@ def ulysses_shard_amax(K, V, k_smoothing=False, out=None, scratch=None):
     return out
 
 
-def ulysses_pack_nvfp4(Q, K, V, P, amax_kv, scale_search=False, k_smoothing=False, send=None):
-    """kvq_ulysses_pack_nvfp4: shard -> send buffer with K/V as NVFP4 under the GLOBAL amax_kv."""
+def ulysses_pack_nvfp4(Q, K, V, P, amax_kv, scale_search=False, k_smoothing=False, send=None, amax_q=None):
+    """kvq_ulysses_pack_nvfp4: shard -> send buffer with K/V (and Q when amax_q is given) as NVFP4 under
+    the GLOBAL amaxes."""
     Ts, H, d = Q.shape
-    sizes = [ulysses_nvfp4_bytes(Ts, H, d, P, p, Q.dtype, k_smoothing) for p in range(P)]
+    sizes = [ulysses_nvfp4_bytes(Ts, H, d, P, p, Q.dtype, k_smoothing, amax_q is not None) for p in range(P)]
     if send is None:
         send = torch.empty(sum(sizes), dtype=torch.uint8, device=Q.device)
     _check(lib().kvq_ulysses_pack_nvfp4(_ptr(Q), _ptr(K), _ptr(V), _dt(Q), Ts, H, d, P, _ptr(amax_kv),
-                                        int(bool(scale_search)), int(bool(k_smoothing)), _ptr(send), _stream()),
-           "kvq_ulysses_pack_nvfp4")
+                                        _ptr(amax_q) if amax_q is not None else None, int(bool(scale_search)),
+                                        int(bool(k_smoothing)), _ptr(send), _stream()), "kvq_ulysses_pack_nvfp4")
     return send, sizes
 
 
@@ -444,11 +478,13 @@ class Ulysses:
     """
 
     def __init__(self, cache: KVCache, H, d, T_c, rank, world, group=None, dtype=torch.bfloat16, nvfp4_kv=False,
-                 peer=False):
+                 peer=False, nvfp4_q=False):
         """nvfp4_kv (§8(f) f3): ship K/V as NVFP4 bytes quantized on the sender with
         the all-reduced global amax (one extra tiny NCCL all-reduce; ~3.6x less K/V volume).
         peer (§8(f) f4): the same payload moved by the kernels themselves over NVLink peer memory
-        (torch symmetric memory windows; no NCCL on the data path)."""
+        (torch symmetric memory windows; no NCCL on the data path).
+        nvfp4_q (with nvfp4_kv): Q is cast to NVFP4 before the all-to-all too -- the
+        attention then sees the quantized Q (a different numerics mode, reading Z24)."""
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.cache, self.H, self.d, self.T_c = cache, H, d, T_c
@@ -485,8 +521,6 @@ class Ulysses:
             wb = peer_window_bytes(T_c, H, d, world, dtype, cache.k_smoothing)
             self.win = symm_mem.empty(wb, dtype=torch.uint8, device=dev)
             self.win.zero_()
-            if not symm_mem.is_symm_mem_enabled_for_group(grp.group_name):
-                symm_mem.enable_symm_mem_for_group(grp.group_name)
             hdl = symm_mem.rendezvous(self.win, grp)
             self.peer = PeerExchange(T_c, H, d, world, rank, list(hdl.buffer_ptrs), dtype, cache.scale_search,
                                      cache.k_smoothing, device=dev)
@@ -494,11 +528,16 @@ class Ulysses:
             torch.cuda.synchronize(dev)
             dist.barrier(group=grp)
         # K-smoothing needs the amax of K_bar, which the bf16 exchange's piggybacked shard amax is not
-        self.nvfp4_kv = bool(nvfp4_kv) or cache.k_smoothing
+        self.nvfp4_q = bool(nvfp4_q)
+        self.nvfp4_kv = bool(nvfp4_kv) or cache.k_smoothing or self.nvfp4_q
         if self.nvfp4_kv:
-            sm = cache.k_smoothing
-            self.nv_send_sizes = [ulysses_nvfp4_bytes(self.Ts, H, d, world, p, dtype, sm) for p in range(world)]
-            self.nv_recv_seg = ulysses_nvfp4_bytes(self.Ts, H, d, world, rank, dtype, sm)
+            sm, qn = cache.k_smoothing, self.nvfp4_q
+            self.nv_send_sizes = [ulysses_nvfp4_bytes(self.Ts, H, d, world, p, dtype, sm, qn) for p in range(world)]
+            self.nv_recv_seg = ulysses_nvfp4_bytes(self.Ts, H, d, world, rank, dtype, sm, qn)
+            self.amax3 = torch.empty(3, dtype=torch.float32, device=dev)  # [K, V, Q] all-reduced together
+            if qn:
+                self.Q16 = torch.empty((T_c, self.Hr, d), dtype=torch.float16, device=dev)
+                self.q_scale = torch.empty(1, dtype=torch.float32, device=dev)
             self.nv_send = torch.empty(sum(self.nv_send_sizes), dtype=torch.uint8, device=dev)
             self.nv_recv = torch.empty(self.nv_recv_seg * world, dtype=torch.uint8, device=dev)
             self.amax_scratch = torch.empty(int(lib().kvq_ulysses_shard_scratch_bytes(self.Ts, H)), dtype=torch.uint8,
@@ -538,17 +577,24 @@ class Ulysses:
             self._mark("o_pull")
             return out
         if self.nvfp4_kv:
-            c = self.cache
-            ulysses_shard_amax(K, V, c.k_smoothing, out=self.amax, scratch=self.amax_scratch)
+            c, qn = self.cache, self.nvfp4_q
+            ulysses_shard_amax(K, V, c.k_smoothing, out=self.amax3[:2], scratch=self.amax_scratch)
+            if qn:
+                ulysses_q_amax(Q, out=self.amax3[2:], scratch=self.amax_scratch)
             self._mark("shard_amax")
-            self.dist.all_reduce(self.amax, op=self.dist.ReduceOp.MAX, group=self.group)
+            self.dist.all_reduce(self.amax3, op=self.dist.ReduceOp.MAX, group=self.group)
             self._mark("amax_allreduce")
-            ulysses_pack_nvfp4(Q, K, V, self.P, self.amax, c.scale_search, c.k_smoothing, send=self.nv_send)
+            aq = self.amax3[2:] if qn else None
+            ulysses_pack_nvfp4(Q, K, V, self.P, self.amax3, c.scale_search, c.k_smoothing, send=self.nv_send, amax_q=aq)
             self._mark("quantize_pack")
             self.dist.all_to_all_single(self.nv_recv, self.nv_send, output_split_sizes=[self.nv_recv_seg] * self.P,
                                         input_split_sizes=self.nv_send_sizes, group=self.group)
             self._mark("a2a_in")
-            c.append_ulysses_nvfp4(layer, chunk_index, self.nv_recv, self.P, self.amax, Q_out=self.Q)
+            if qn:
+                c.append_ulysses_nvfp4(layer, chunk_index, self.nv_recv, self.P, self.amax3, q_dtype=Q.dtype,
+                                       Q_out=self.Q16, amax_q=aq, q_scale=self.q_scale)
+            else:
+                c.append_ulysses_nvfp4(layer, chunk_index, self.nv_recv, self.P, self.amax3, Q_out=self.Q)
             self._mark("scatter_append")
             return self._attend_and_return(layer, mask, out, Q)
         _check(L.kvq_ulysses_pack_qkv(_ptr(Q), _ptr(K), _ptr(V), dt, self.Ts, self.H, self.d, self.P,
@@ -566,7 +612,10 @@ class Ulysses:
 
     def _attend_and_return(self, layer, mask, out, Q):
         L, st = lib(), _stream()
-        self.cache.attention(layer, self.Q, mask, out=self.O_local)
+        if self.nvfp4_q:
+            self.cache.attention_qscaled(layer, self.Q16, self.q_scale, mask, out=self.O_local)
+        else:
+            self.cache.attention(layer, self.Q, mask, out=self.O_local)
         self._mark("attention")
         o_send = self.O_local.view(torch.uint8).reshape(-1)
         self.dist.all_to_all_single(self.o_recv, o_send, output_split_sizes=self.o_recv_sizes,

@@ -154,3 +154,26 @@ def test_cache_keys_follow_ranges_across_chunks():
     # frames {0} U {3, 4, 5} -> tokens [0,4) U [12,24)
     ref = np.concatenate([raw[0][0:4], raw[1][4:8], raw[2]])
     assert np.array_equal(Kk, ref)
+
+
+def test_q_nvfp4_mode_is_identity_on_lattice_queries_and_quantizes_otherwise():
+    # reading Z24 (NVFP4 Q before the all-to-all): queries already on the NVFP4 lattice
+    # (g = 2^-8, a +-6 in every block so the scale is recovered) pass through unchanged; other queries
+    # are replaced by their exact dequantized NVFP4 values
+    T, H, d = 16, 2, 32
+    rng = np.random.default_rng(7)
+    c = OracleKVCache(1, H, d, T, 1)
+    k = synth.make_tensor((T, H, d), "fp32", seed=11).f64
+    v = synth.make_tensor((T, H, d), "fp32", seed=12).f64
+    c.append(0, 0, k, v)
+    mags = np.array([0, 0.5, 1, 1.5, 2, 3, 4, 6])
+    e = rng.choice(mags, size=(T * H, d // 16, 16)) * rng.choice([-1, 1], size=(T * H, d // 16, 16))
+    e[:, :, 0] = 6.0
+    s = nvfp4.e4m3_decode(rng.integers(40, 110, size=(T * H, d // 16)).astype(np.uint8))
+    s[0, 0] = 448.0
+    q_lat = (e * s[..., None] * 2.0 ** -8).reshape(T, H, d)
+    np.testing.assert_array_equal(c.attend(0, 0, q_lat, 0, 1, q_nvfp4=True), c.attend(0, 0, q_lat, 0, 1))
+    q = synth.make_tensor((T, H, d), "fp32", seed=13).f64
+    q_hat = nvfp4.dequantize_kv_chunk(nvfp4.quantize_kv_chunk(q), T, H, d)
+    assert not np.array_equal(q_hat, q)
+    np.testing.assert_array_equal(c.attend(0, 0, q, 0, 1, q_nvfp4=True), attention(q_hat, *c.keys(0, 0, 0, 1)))
