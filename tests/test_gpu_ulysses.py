@@ -292,3 +292,43 @@ def test_ulysses_nvfp4_q_mode_simulated(P, H):
                 full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
                 assert torch.equal(e[name], full), (p, name)
         check_fp32_out(O_full.cpu().numpy(), orc.attend(0, ch, q.f64, sink, window, q_nvfp4=True))
+
+
+def test_ulysses_nvfp4_exchange_wan_shape_p8():
+    # BASELINE.json configs[4] shape: the Wan layer (12 x 128, T_c = 4680) head-sharded over P = 8
+    # simulated ranks (2,2,2,2,1,1,1,1 heads), NVFP4 exchange: every rank's cache bytes equal the
+    # 1-GPU cache's; sampled O rows within tolerance of the oracle
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    P, H, d, tpf, fc = 8, 12, 128, 1560, 3
+    T = tpf * fc
+    Ts = T // P
+    parts = [kvq.head_partition(H, P, r) for r in range(P)]
+    mk = dict(sink_frames=3, window_frames=21, max_chunk_slots=8, device=DEV)
+    caches = [kvq.KVCache(1, h1 - h0, d, tpf, fc, **mk) for h0, h1 in parts]
+    ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    orc = OracleKVCache(1, H, d, tpf, fc)
+    rows = np.array([0, 584, 585, 2047, 4095, 4679])
+    for ch in range(3):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch)
+        Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+        mask = kvq.Mask(ch, 3, 21)
+        ref.append(0, ch, K, V)
+        orc.append(0, ch, k.f64, v.f64)
+        shards = [tuple(x[r * Ts:(r + 1) * Ts].contiguous() for x in (Q, K, V)) for r in range(P)]
+        amax = torch.stack([kvq.ulysses_shard_amax(Kr, Vr) for _, Kr, Vr in shards]).max(0).values
+        packed = [kvq.ulysses_pack_nvfp4(Qr, Kr, Vr, P, amax) for Qr, Kr, Vr in shards]
+        recv = _a2a([sd for sd, _ in packed], [sz for _, sz in packed], None)
+        O_locals = []
+        for p, (h0, h1) in enumerate(parts):
+            Ql = caches[p].append_ulysses_nvfp4(0, ch, recv[p], P, amax)
+            O_locals.append(caches[p].attention(0, Ql, mask, torch.float32))
+        ex = ref.export(0, ch)
+        for p, (h0, h1) in enumerate(parts):
+            e = caches[p].export(0, ch)
+            for name in ("codes_k", "scales_k", "codes_v", "scales_v"):
+                full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
+                assert torch.equal(e[name], full), (p, name)
+        if ch == 2:
+            O = torch.cat([O_locals[p] for p in range(P)], dim=1).cpu().numpy()   # [T, H, d] by head blocks
+            check_fp32_out(O[rows], orc.attend(0, ch, q.f64, 3, 21, rows=rows))
