@@ -360,3 +360,37 @@ def test_resident_footprint_ratio():
     nv = c.resident_bytes()
     assert nv == nvfp4.storage_bytes(T, H, d)
     assert abs((4 * T * H * d) / (nv - 8) - 32 / 9) < 1e-12
+
+
+def test_probe_e2m1_encode_exhaustive_binades():
+    # SURVEY.md §4 item 2 (day-1 codec probe): cvt.rn.satfinite.e2m1x2.f32 against the oracle on EVERY
+    # fp32 value in [2^-3, 2^3) and its negative (all E2M1 decision boundaries lie there; below is 0,
+    # above saturates), 16M values per call
+    _gpu()
+    bad = 0
+    for e in range(-3, 3):
+        m = np.arange(1 << 23, dtype=np.uint32)
+        for sign in (0, 1):
+            bits = (np.uint32(sign << 31) | np.uint32((e + 127) << 23) | m).view(np.float32)
+            got = kvq.probe(0, torch.from_numpy(bits).to(DEV), bits.size // 2).cpu().numpy()
+            want = nvfp4.e2m1_encode(bits.astype(np.float64))
+            bad += int(np.count_nonzero(got != want))
+    assert bad == 0
+
+
+def test_probe_e4m3_encode_near_every_midpoint_and_strided():
+    # cvt.rn.satfinite.e4m3x2.f32 against the oracle: +-64 fp32 ulps around every midpoint between
+    # adjacent E4M3 values (the only places rounding can go wrong) plus every 16th fp32 pattern in
+    # [2^-12, 2^9)
+    _gpu()
+    v = nvfp4.e4m3_decode(np.arange(0x7F))
+    mids = ((v[1:] + v[:-1]) / 2).astype(np.float32)
+    near = (mids.view(np.uint32)[:, None].astype(np.int64) + np.arange(-64, 65)[None, :]).reshape(-1)
+    strided = np.arange((127 - 12) << 23, (127 + 9) << 23, 16, dtype=np.int64)
+    x = np.concatenate([near, strided]).astype(np.uint32).view(np.float32)
+    bad = 0
+    for i in range(0, x.size, 1 << 24):
+        xs = x[i:i + (1 << 24)]
+        got = kvq.probe(1, torch.from_numpy(xs.copy()).to(DEV), xs.size).cpu().numpy()
+        bad += int(np.count_nonzero(got != nvfp4.e4m3_encode_nonneg(xs.astype(np.float64))))
+    assert bad == 0
