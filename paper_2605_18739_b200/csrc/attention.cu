@@ -27,6 +27,7 @@
 // (tcgen05.commit for MMA completion); MMAs execute in issue order, so the commit that signals
 // S_i(j+1) also guarantees PV_i(j) finished (O_i stable for the rescale, P_i(j) consumed).
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -680,6 +681,371 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #undef SQL
 }
 
+// ---------------------------------------------------------------------------------------------
+// v2 (d = 128, NVFP4 cache, bf16 queries, plain mode): 64-key tiles so that each query tile's P has
+// TMEM columns of its own -- S_i [64 i, +64), P_i [128 + 32 i, +32), O_i [256 + 128 i, +128) -- and
+// QK_i(j+1) is issued as soon as softmax_i(j) has loaded S_i(j) into registers (the `sfree` barrier),
+// overlapping the next scores with this tile's softmax.  The tensor core then runs
+// QK0(j) QK1(j) PV0(j-1) PV1(j-1) ...; softmax_i(j) waits for PV_i(j-1) (`pempty`) only before it
+// writes P_i(j) and rescales O_i.  Dequant: 64 threads per tensor (one key row each).
+constexpr int kV2Keys = 64;
+struct V2Smem {
+  static constexpr int kQ = 128 * 128 * 2;   // one 128-query tile (bytes)
+  static constexpr int kKV = 64 * 128 * 2;   // one 64-key tile
+  static constexpr int kQ0 = 0, kQ1 = kQ;
+  static constexpr int kK0 = 2 * kQ, kK1 = kK0 + kKV, kV0 = kK1 + kKV, kV1 = kV0 + kKV;
+  static constexpr int kBar = kV1 + kKV;
+  static constexpr int kBytes = kBar + 24 * 8 + 16 + 1024;
+};
+
+KVQ_DEV uint32_t chunk_addr64(uint32_t base, int r, int c) {  // 64-row K-major SW128 tile
+  return base + (uint32_t)(c >> 3) * 8192u + sw128_off(r, c & 7);
+}
+
+template <int D>
+KVQ_DEV void store_dequant_row64(uint32_t base, int r, const PackedRow<D>& pr) {
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) {
+    const uint32_t sb = (pr.s[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t s2 = f16x2_from_e4m3x2(sb | (sb << 8));
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int wi = 2 * j + half;
+      const uint4 q = pr.c[wi >> 2];
+      const uint32_t w = (wi & 3) == 0 ? q.x : (wi & 3) == 1 ? q.y : (wi & 3) == 2 ? q.z : q.w;
+      uint32_t o[4];
+      dequant_word_f16(w, s2, o);
+      st_shared_v4(chunk_addr64(base, r, wi), o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+KVQ_DEV int count_tiles64(const AttnParams& p) {
+  int n = 0;
+  for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 63) >> 6) - (p.seg[s].begin >> 6);
+  return n;
+}
+KVQ_DEV void tile_seek64(const AttnParams& p, int tb, TileIter& it) {
+  int s = 0;
+  for (; s < p.nseg; ++s) {
+    const int nt = ((p.seg[s].end + 63) >> 6) - (p.seg[s].begin >> 6);
+    if (tb < nt) break;
+    tb -= nt;
+  }
+  it.seg = s;
+  it.t0 = (p.seg[s].begin & ~63) + 64 * tb;
+}
+KVQ_DEV void tile_next64(const AttnParams& p, TileIter& it) {
+  it.t0 += 64;
+  if (it.t0 < p.seg[it.seg].end) return;
+  if (++it.seg >= p.nseg) return;
+  it.t0 = p.seg[it.seg].begin & ~63;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_constant__ AttnParams p) {
+  static_assert(D == 128, "v2: d = 128");
+  using SM = V2Smem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+#define V2Q(i) (sbase + SM::kQ0 + (uint32_t)(i) * SM::kQ)
+#define V2K(b) (sbase + SM::kK0 + (uint32_t)(b) * SM::kKV)
+#define V2V(b) (sbase + SM::kV0 + (uint32_t)(b) * SM::kKV)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+  uint64_t* kfull = bars + 0;    // [2] dequant -> MMA (64 arrivals)
+  uint64_t* vfull = bars + 2;    // [2]
+  uint64_t* kempty = bars + 4;   // [2] MMA -> dequant
+  uint64_t* vempty = bars + 6;   // [2]
+  uint64_t* sfull = bars + 8;    // [2] MMA -> softmax i: S_i(j) ready
+  uint64_t* sfree = bars + 10;   // [2] softmax i -> MMA: S_i(j) loaded, its columns may be overwritten
+  uint64_t* pfull = bars + 12;   // [2] softmax i -> MMA: P_i(j) written, O_i rescaled
+  uint64_t* pempty = bars + 14;  // [2] MMA -> softmax i: PV_i(j) done (P_i free, O_i stable)
+  uint64_t* ofull = bars + 16;   // [2] MMA -> softmax i: last PV_i of a piece done
+  uint64_t* qfull = bars + 18;   // [2] softmax i -> MMA: Q_i of a piece loaded
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int H = p.H;
+  const int n = count_tiles64(p);
+  const int64_t W = (int64_t)p.units * n;
+  const int G = gridDim.x, c = blockIdx.x;
+
+  if (warp == 12) tmem_alloc(tslot, 512);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(kfull + b, 64);
+      mbar_init(vfull + b, 64);
+      mbar_init(kempty + b, 1);
+      mbar_init(vempty + b, 1);
+      mbar_init(sfull + b, 1);
+      mbar_init(sfree + b, 128);
+      mbar_init(pfull + b, 128);
+      mbar_init(pempty + b, 1);
+      mbar_init(ofull + b, 1);
+      mbar_init(qfull + b, 128);
+    }
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp < 8) {
+    // ================================================================ softmax WG (query tile qi)
+    reg_alloc<kRegSoftmax>();
+    const int qi = warp >> 2;
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + 64 * qi + lane_off;
+    const uint32_t tP = tmem + 128 + 32 * qi + lane_off;
+    const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
+    const float sl2 = p.scale_log2;
+    int g = 0;   // tiles processed (barrier parity)
+    int kk = 0;  // pieces processed
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k, ++kk) {
+      const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
+      const int t = q0 + 128 * qi + row;
+      (void)load_q_row<D, false, false, false>(V2Q(qi), V2Q(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      fence_proxy_async_smem();
+      mbar_arrive(qfull + qi);
+      float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
+      TileIter it;
+      tile_seek64(p, pc.tb, it);
+      for (int j = 0; j < pc.te - pc.tb; ++j, ++g, tile_next64(p, it)) {
+        const AttnSeg& sg = p.seg[it.seg];
+        const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, kV2Keys);
+        const float gk = __ldg(p.g + 2 * sg.slot), gv = __ldg(p.g + 2 * sg.slot + 1);
+        const float cs = gk * sl2;
+        mbar_wait(sfull + qi, g & 1);
+        tc_fence_after();
+        uint32_t s[64];
+        KVQ_TMEM_LD32(tS, s);
+        KVQ_TMEM_LD32(tS + 32, (s + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(sfree + qi);  // QK_i(j+1) may now overwrite S_i
+        if (lo != 0 || hi != kV2Keys) {
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            if (q < lo || q >= hi) s[q] = __float_as_uint(-INFINITY);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 64; q += 8) {
+          mx0 = fmax3(mx0, __uint_as_float(s[q]), __uint_as_float(s[q + 1]));
+          mx1 = fmax3(mx1, __uint_as_float(s[q + 2]), __uint_as_float(s[q + 3]));
+          mx2 = fmax3(mx2, __uint_as_float(s[q + 4]), __uint_as_float(s[q + 5]));
+          mx3 = fmax3(mx3, __uint_as_float(s[q + 6]), __uint_as_float(s[q + 7]));
+        }
+        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * cs;
+        const float m_new = (j == 0 || m_tile > m_run + kLazyLog2) ? fmaxf(m_run, m_tile) : m_run;
+        const float alpha = ex2_approx(m_run - m_new);
+        const uint64_t cs2 = f32x2_pack(cs, cs), mneg2 = f32x2_pack(-m_new, -m_new);
+        float la[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const uint64_t x2 = ffma2(f32x2_pack(__uint_as_float(s[2 * q]), __uint_as_float(s[2 * q + 1])), cs2, mneg2);
+          float x0, x1, p0, p1;
+          f32x2_unpack(x2, x0, x1);
+          if ((q & 7) < kPolyPairs) {
+            exp2_poly_pair(x0, x1, p0, p1);
+          } else {
+            p0 = ex2_approx(x0);
+            p1 = ex2_approx(x1);
+          }
+          const uint32_t pk = pack_half2(p0, p1);
+          s[q] = pk;
+          asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.f16 %0, l, %0;\n add.rn.f32.f16 %1, h, %1;\n}"
+              : "+f"(la[(q & 1) * 2]), "+f"(la[(q & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
+        }
+        l_run = l_run * alpha + ((la[0] + la[1]) + (la[2] + la[3]));
+        // PV_i(j-1) done: P_i free, O_i stable (the first tile of a piece waits for the previous piece's)
+        if (g > 0) mbar_wait(pempty + qi, (g - 1) & 1);
+        tc_fence_after();
+        KVQ_TMEM_ST32(tP, s);
+        if (j > 0) {
+          const float f = alpha * (gv_run / gv);
+          if (!__all_sync(0xffffffffu, f == 1.0f)) {
+            const uint64_t f2 = f32x2_pack(f, f);
+            uint32_t o[64];
+#pragma unroll
+            for (int cc = 0; cc < D / 32; cc += 2) {
+              KVQ_TMEM_LD32(tO + 32 * cc, o);
+              KVQ_TMEM_LD32(tO + 32 * (cc + 1), (o + 32));
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 64; q += 2) {
+                float x0, x1;
+                f32x2_unpack(fmul2(f32x2_pack(__uint_as_float(o[q]), __uint_as_float(o[q + 1])), f2), x0, x1);
+                o[q] = __float_as_uint(x0);
+                o[q + 1] = __float_as_uint(x1);
+              }
+              KVQ_TMEM_ST32(tO + 32 * cc, o);
+              KVQ_TMEM_ST32(tO + 32 * (cc + 1), (o + 32));
+            }
+          }
+        }
+        gv_run = gv;
+        m_run = m_new;
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(pfull + qi);
+      }
+      // ---- piece epilogue
+      mbar_wait(ofull + qi, kk & 1);
+      tc_fence_after();
+      const float f = pc.full ? gv_run / l_run : gv_run;
+      float* wsO = p.ws + (size_t)pc.slot * p.ws_slot_floats + (size_t)(128 * qi + row) * D;
+      if (!pc.full && t < p.Tq) {
+        float* wml = p.ws + (size_t)pc.slot * p.ws_slot_floats + 256 * D;
+        wml[128 * qi + row] = m_run;
+        wml[256 + 128 * qi + row] = l_run;
+      }
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        KVQ_TMEM_LD32(tO + 32 * cc, o);
+        tmem_ld_wait();
+        if (t < p.Tq) {
+          if (!pc.full) {
+            float4* dst = reinterpret_cast<float4*>(wsO + 32 * cc);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[q] = make_float4(__uint_as_float(o[4 * q]) * f, __uint_as_float(o[4 * q + 1]) * f,
+                                   __uint_as_float(o[4 * q + 2]) * f, __uint_as_float(o[4 * q + 3]) * f);
+          } else {
+            const int64_t base = ((int64_t)t * H + h) * D + 32 * cc;
+            if (p.out_dtype == DT_FP32) {
+              float4* dst = reinterpret_cast<float4*>((float*)p.O + base);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                dst[q] = make_float4(__uint_as_float(o[4 * q]) * f, __uint_as_float(o[4 * q + 1]) * f,
+                                     __uint_as_float(o[4 * q + 2]) * f, __uint_as_float(o[4 * q + 3]) * f);
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.O + base);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(pack_bf162(__uint_as_float(o[8 * q]) * f, __uint_as_float(o[8 * q + 1]) * f),
+                                    pack_bf162(__uint_as_float(o[8 * q + 2]) * f, __uint_as_float(o[8 * q + 3]) * f),
+                                    pack_bf162(__uint_as_float(o[8 * q + 4]) * f, __uint_as_float(o[8 * q + 5]) * f),
+                                    pack_bf162(__uint_as_float(o[8 * q + 6]) * f, __uint_as_float(o[8 * q + 7]) * f));
+            }
+          }
+        }
+      }
+    }
+  } else if (warp < 12) {
+    // ================================================================ dequant WG: 64 K rows + 64 V rows
+    reg_dealloc<kRegDequant>();
+    const int r = (tid - 256) & 63;
+    const bool is_v = tid - 256 >= 64;
+    uint64_t* full = is_v ? vfull : kfull;
+    uint64_t* empty = is_v ? vempty : kempty;
+    const uint8_t* codes = is_v ? p.codes_v : p.codes_k;
+    const uint8_t* scales = is_v ? p.scales_v : p.scales_k;
+    int g = 0;
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+      const int h = pc.unit / p.qpairs;
+      TileIter it;
+      tile_seek64(p, pc.tb, it);
+      for (int j = pc.tb; j < pc.te; ++j, ++g, tile_next64(p, it)) {
+        const AttnSeg& sg = p.seg[it.seg];
+        const int b = g & 1;
+        const int64_t crow = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
+        PackedRow<D> pr;
+        load_packed_row<D>(pr, codes + crow * (D / 2), scales + crow * (D / 16));
+        if (g >= 2) mbar_wait(empty + b, ((g >> 1) - 1) & 1);
+        store_dequant_row64<D>(is_v ? V2V(b) : V2K(b), r, pr);
+        fence_proxy_async_smem();
+        mbar_arrive(full + b);
+      }
+    }
+  } else {
+    reg_dealloc<kRegMma>();
+  }
+  if (warp == 12) {
+    // ================================================================ MMA issuer warp
+    constexpr uint32_t kIdS = umma_idesc_f16(128, kV2Keys, 0, 0, 0);
+    constexpr uint32_t kIdO = umma_idesc_f16(128, D, 0, 0, 1);
+    const uint64_t dQ0 = umma_desc_sw128(V2Q(0), 16, 1024), dQ1 = umma_desc_sw128(V2Q(1), 16, 1024);
+    const uint64_t dK0 = umma_desc_sw128(V2K(0), 16, 1024), dK1 = umma_desc_sw128(V2K(1), 16, 1024);
+    const uint64_t dV0 = umma_desc_sw128(V2V(0), 8192, 1024), dV1 = umma_desc_sw128(V2V(1), 8192, 1024);
+    auto issue_qk = [&](int qi, int b) {
+      const uint64_t da = qi ? dQ1 : dQ0, db = b ? dK1 : dK0;
+      const uint32_t dt = tmem + 64u * qi;
+      if (elect_one()) {
+#pragma unroll
+        for (int q = 0; q < D / 16; ++q)
+          umma_ss(dt, da + (uint64_t)(((q >> 2) * 16384 + (q & 3) * 32) >> 4),
+                  db + (uint64_t)(((q >> 2) * 8192 + (q & 3) * 32) >> 4), kIdS, q > 0 ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int qi, int b, bool first) {
+      const uint64_t db = b ? dV1 : dV0;
+      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + 128u + 32u * qi;
+      if (elect_one()) {
+#pragma unroll
+        for (int q = 0; q < kV2Keys / 16; ++q)
+          umma_ts(dt, ta + 8 * q, db + (uint64_t)((q * 2048) >> 4), kIdO, (!first || q > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) kvq::tc_commit(bar);
+      __syncwarp();
+    };
+    auto pv_pair = [&](int t, bool first, bool last) {  // PV of global tile t for both query tiles
+      const int bt = t & 1;
+      mbar_wait(vfull + bt, (t >> 1) & 1);
+      mbar_wait(pfull + 0, t & 1);
+      tc_fence_after();
+      issue_pv(0, bt, first);
+      commit(pempty + 0);
+      if (last) commit(ofull + 0);
+      mbar_wait(pfull + 1, t & 1);
+      tc_fence_after();
+      issue_pv(1, bt, first);
+      commit(pempty + 1);
+      if (last) commit(ofull + 1);
+      commit(vempty + bt);
+    };
+    int g = 0;
+    Piece pc;
+    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+      const int np = pc.te - pc.tb;
+      mbar_wait(qfull + 0, k & 1);
+      mbar_wait(qfull + 1, k & 1);
+      for (int j = 0; j < np; ++j) {
+        const int gj = g + j, b = gj & 1;
+        mbar_wait(kfull + b, (gj >> 1) & 1);
+        if (gj > 0) mbar_wait(sfree + 0, (gj - 1) & 1);
+        tc_fence_after();
+        issue_qk(0, b);
+        commit(sfull + 0);
+        if (gj > 0) mbar_wait(sfree + 1, (gj - 1) & 1);
+        tc_fence_after();
+        issue_qk(1, b);
+        commit(sfull + 1);
+        commit(kempty + b);
+        if (j > 0) pv_pair(gj - 1, j == 1, false);
+      }
+      pv_pair(g + np - 1, np == 1, true);
+      g += np;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) tmem_dealloc(tmem, 512);
+#undef V2Q
+#undef V2K
+#undef V2V
+}
+
 // Merge the partial pieces of every split unit: O = sum_p 2^(m_p - m) O_p / sum_p 2^(m_p - m) l_p,
 // pieces in increasing CTA order (deterministic).  A unit is split exactly when a CTA range boundary
 // falls strictly inside it; CTA b of this kernel handles the boundary of attention CTA b (if it is
@@ -766,9 +1132,49 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// v2 is opt-in (environment KVQ_ATTN_V2=1): correct (parity tests), but 945 us against v1's 850 on
+// the Wan layer -- the per-tile softmax overheads double with 64-key tiles
+bool attn_v2_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KVQ_ATTN_V2");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
+
+cudaError_t launch_v2(AttnParams p, cudaStream_t st) {
+  auto kern = attn_v2_kernel<128>;
+  const int smem = V2Smem::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  p.qpairs = (p.Tq + 255) / 256;
+  p.units = p.qpairs * p.H;
+  int n = 0;
+  for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 63) >> 6) - (p.seg[s].begin >> 6);
+  if (n == 0 || p.units == 0) return cudaSuccess;
+  int G = p.units;
+  bool split = false;
+  if (p.ws != nullptr && p.ws_slots >= 2) {
+    G = p.ws_slots / 2 < p.max_ctas ? p.ws_slots / 2 : p.max_ctas;
+    const int64_t W = (int64_t)p.units * n;
+    if (G > W / 2) G = (int)(W / 2);
+    if (G < 1) G = 1;
+    split = (W % G != 0) || ((W / G) % n != 0);
+  }
+  p.grid = G;
+  p.ws_slot_floats = 256 * 128 + 512;
+  kern<<<G, kThreads, smem, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !split) return e;
+  if (G > 1) combine_kernel<128><<<dim3(G - 1, kCombineSplit), 512, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+
 template <int D, bool SMOOTH>
 cudaError_t launch_nvfp4(const AttnParams& p, cudaStream_t st) {
-  return p.q_dtype == DT_FP32 ? launch_t<D, true, false, SMOOTH, true>(p, st) : launch_t<D, true, false, SMOOTH>(p, st);
+  if (p.q_dtype == DT_FP32) return launch_t<D, true, false, SMOOTH, true>(p, st);
+  if (D == 128 && !SMOOTH && p.q_dtype == DT_BF16 && p.q_scale == nullptr && attn_v2_enabled()) return launch_v2(p, st);
+  return launch_t<D, true, false, SMOOTH>(p, st);
 }
 
 }  // namespace

@@ -394,3 +394,39 @@ def test_probe_e4m3_encode_near_every_midpoint_and_strided():
         got = kvq.probe(1, torch.from_numpy(xs.copy()).to(DEV), xs.size).cpu().numpy()
         bad += int(np.count_nonzero(got != nvfp4.e4m3_encode_nonneg(xs.astype(np.float64))))
     assert bad == 0
+
+
+def test_attention_v2_64key_tiles_wan_layer_sampled():
+    # the opt-in 64-key-tile attention (KVQ_ATTN_V2=1, read once per process): run in a subprocess so
+    # the default path of this process is untouched; Wan layer, sampled rows vs the oracle
+    _gpu()
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch
+from oracle.cache import OracleKVCache
+from paper_2605_18739_b200 import kvq, synth
+import sys
+sys.path.insert(0, 'tests')
+from gpu_util import check_fp32_out, check_bf16_out
+T, H, d = 4680, 12, 128
+c = kvq.KVCache(1, H, d, 1560, 3, sink_frames=3, window_frames=21, max_chunk_slots=8, device='cuda')
+o = OracleKVCache(1, H, d, 1560, 3)
+for ch in range(7):
+    q, k, v = synth.make_qkv(T, H, d, 'bf16', 0, ch)
+    c.append(0, ch, k.torch('cuda'), v.torch('cuda'))
+    o.append(0, ch, k.f64, v.f64)
+rows = np.array([0, 127, 128, 2047, 4095, 4607, 4608, 4679])
+m = kvq.Mask(6, 3, 21)
+O32 = c.attention(0, q.torch('cuda'), m, torch.float32).cpu().numpy()
+ref = o.attend(0, 6, q.f64, 3, 21, rows=rows)
+check_fp32_out(O32[rows], ref)
+Ob = c.attention(0, q.torch('cuda'), m, torch.bfloat16).float().cpu().numpy()
+check_bf16_out(Ob[rows], ref, O32[rows])
+print('ok')
+"""
+    env = dict(os.environ, KVQ_ATTN_V2="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
