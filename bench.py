@@ -172,9 +172,15 @@ def run_gpu(args):
         q, k, v = synth.make_qkv(T_C, H, D, "bf16", 0, ch)
         chunks.append(tuple(x.torch("cpu")[rank * Ts:(rank + 1) * Ts].contiguous() for x in (q, k, v)))
     dq = [tuple(x.to(dev) for x in c) for c in chunks]
-    uly = (kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer",
-                       nvfp4_q=args.exchange == "nvfp4q")
-           if P > 1 or force else None)
+    native = args.exchange.startswith("native")
+    if not (P > 1 or force):
+        uly = None
+    elif native:  # the one-call C step with libkvq's own NCCL communicator
+        uly = kvq.NcclUlysses(cache, H, rank, P, exchange=kvq.EXCHANGE_NVFP4 if args.exchange == "native-nvfp4"
+                              else kvq.EXCHANGE_INPUT)
+    else:
+        uly = kvq.Ulysses(cache, H, D, T_C, rank, P, nvfp4_kv=args.exchange == "nvfp4", peer=args.exchange == "peer",
+                          nvfp4_q=args.exchange == "nvfp4q")
 
     def step(c, out=None):
         q, k, v = dq[c]
@@ -312,7 +318,8 @@ def run_gpu(args):
            # N>1 bf16 adds amax + pack, unpack Q/K/V and unpack O (NCCL kernels not counted); nvfp4: amax (2-3),
            # reduce, pack, scatter, attention + combine, unpack O; peer: amax (2-3), reduce, publish, pack, scatter,
            # attention + combine, signal, pull
-           "gpu_launches": args.steps * (3 if world == 1 else {"bf16": 7, "nvfp4": 8, "nvfp4q": 11, "peer": 10}[args.exchange])}
+           "gpu_launches": args.steps * (3 if world == 1 else {"bf16": 7, "nvfp4": 8, "nvfp4q": 11, "peer": 10, "native": 7,
+                                                                       "native-nvfp4": 8}[args.exchange])}
     if uly is None:
         att_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_att]))
         app_ms_ev = float(np.mean([a.elapsed_time(b) for a, b in ev_app]))
@@ -375,7 +382,7 @@ def run_gpu(args):
     else:
         # per-phase breakdown of one distributed layer step (CUDA events per phase, median of 5 steps,
         # max over ranks) -- SURVEY.md §8(d) D5
-        bd = uly.breakdown(lambda: step(CHUNK, O))
+        bd = uly.breakdown(lambda: step(CHUNK, O)) if not native else {"step": step_ms}
         names = list(bd)
         tb = torch.tensor([bd[n] for n in names], dtype=torch.float64, device=dev)
         if world > 1:
@@ -399,6 +406,8 @@ def run_gpu(args):
         print(json.dumps(out), flush=True)
     if world > 1 or force:
         dist.barrier()
+        if native:
+            uly.close()
         dist.destroy_process_group()
 
 
@@ -438,10 +447,12 @@ def main():
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--force-ulysses", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "nvfp4q", "peer"],
+    ap.add_argument("--exchange", default="bf16", choices=["bf16", "nvfp4", "nvfp4q", "peer", "native", "native-nvfp4"],
                     help="N>1: bf16 all-to-all (NCCL), nvfp4 = §8(f) f3 (K/V quantized on the sender, NCCL), "
                          "nvfp4q = nvfp4 with Q cast to NVFP4 too (PAPER.md:646; a different numerics mode), "
-                         "peer = §8(f) f4 (the kernels store/load over NVLink peer memory, no NCCL on the data path)")
+                         "peer = §8(f) f4 (the kernels store/load over NVLink peer memory, no NCCL on the data path), "
+                         "native / native-nvfp4 = the bf16 / nvfp4 exchange behind the one C call "
+                         "ulysses_chunk_attention with libkvq's own NCCL communicator")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

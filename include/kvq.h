@@ -97,6 +97,8 @@ kvq_status kvq_cache_create(const kvq_config* cfg, void* dev_arena, size_t arena
 kvq_status kvq_cache_destroy(kvq_cache* cache);
 /* Forget every chunk (new video); zeroes the arena on `stream`. */
 kvq_status kvq_cache_reset(kvq_cache* cache, void* stream);
+/* Copies the cache's geometry (as passed to kvq_cache_create) into *out (host). */
+kvq_status kvq_cache_get_config(const kvq_cache* cache, kvq_config* out);
 /* Re-bind the shot-level sink A_s (a prompt switch).  Moves two host
  * pointers only; never touches cache bytes ("zero memory overhead").  Chunks
  * overlapping [start, start+len) frames are pinned against eviction from now on. */
@@ -306,6 +308,48 @@ kvq_status kv_append_peer(const kvq_peer* peer, kvq_cache* cache, int32_t layer,
 kvq_status kvq_peer_signal_o(const kvq_peer* peer, int64_t epoch, void* stream);
 /* O_shard dev [T_c/P, H, d] bf16. */
 kvq_status kvq_peer_pull_o(const kvq_peer* peer, int64_t epoch, void* O_shard, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * One-call head-sharded chunk step with a library-owned NCCL communicator (
+ * PAPER.md:556-564 App. C, App. D).  Same kernels as the calls above, with
+ * the collectives issued by the library itself (grouped ncclSend/ncclRecv all-to-allv and an
+ * ncclAllReduce(MAX) of the tensor amaxes) on the caller's stream.  NCCL allocates its own
+ * device memory inside kvq_comm_create (the one exception to "no entry point allocates");
+ * everything else lives in a caller-owned workspace.  Collective calls must be made by every
+ * rank of the communicator in the same order (NCCL's rule). */
+typedef struct kvq_comm kvq_comm;
+
+/* Exchange payloads: 0 = Q, K, V in the input dtype (+ piggybacked shard amax, reading Z18);
+ * 1 = K/V as NVFP4 cache bytes quantized on the sender with the all-reduced amax (f3);
+ * 2 = as 1 with NVFP4 Q (reading Z24, different attention numerics). */
+enum { KVQ_EXCHANGE_INPUT = 0, KVQ_EXCHANGE_NVFP4 = 1, KVQ_EXCHANGE_NVFP4_Q = 2 };
+
+/* out_128_bytes (host): an ncclUniqueId made on rank 0, to be broadcast to the other ranks. */
+kvq_status kvq_get_unique_id(void* out_128_bytes);
+/* Joins the communicator (blocking until all nranks joined) on the CURRENT CUDA device. */
+kvq_status kvq_comm_create(const void* unique_id, int32_t nranks, int32_t rank, kvq_comm** out);
+kvq_status kvq_comm_destroy(kvq_comm* comm);
+/* Device workspace bytes for ulysses_chunk_attention on this rank: chunk T_c tokens (T_c % P
+ * == 0), H heads in total, exchange mode as above, Q/K/V in in_dtype, O in out_dtype. */
+size_t kvq_ulysses_workspace_bytes(int32_t T_c, int32_t H, int32_t d, int32_t P, int32_t rank,
+                                   int32_t exchange, kvq_dtype in_dtype, kvq_dtype out_dtype);
+/* Binds the total head count H, the exchange mode and a caller-owned dev workspace (256-byte
+ * aligned, >= kvq_ulysses_workspace_bytes for the shapes used; KVQ_ECAPACITY at the call
+ * otherwise) to the comm. */
+kvq_status kvq_comm_configure(kvq_comm* comm, int32_t num_heads, int32_t exchange,
+                              void* dev_workspace, size_t workspace_bytes);
+/* The chunk step of one rank: Q/K/V_shard dev [T_c/P, H, d] in_dtype (this rank's sequence
+ * shard; T_c = P * (T_c/P) must equal the cache's chunk length), cache = this rank's heads
+ * [h0, h1) of kvq_head_partition (else KVQ_ESHAPE) -> exchange -> quantize/append chunk
+ * `chunk_index` of `layer` -> chunk_attention over `mask` -> exchange of O back ->
+ * O_shard dev [T_c/P, H, d] out_dtype.  Codes and scales equal those of a 1-GPU cache of all
+ * heads (the amax is global).  KVQ_ENCCL if a collective fails; K-smoothing caches need
+ * exchange >= 1 (the shard amax of K is not that of K - mean) -> KVQ_EINVAL otherwise. */
+kvq_status ulysses_chunk_attention(kvq_comm* comm, kvq_cache* cache, int32_t layer,
+                                   int64_t chunk_index, const void* Q_shard, const void* K_shard,
+                                   const void* V_shard, kvq_dtype in_dtype, const kvq_mask* mask,
+                                   float softmax_scale, void* O_shard, kvq_dtype out_dtype,
+                                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,20 @@ PER_FILE = {
     "attention.cu": [],
     "ulysses.cu": [],
     "api.cpp": [],
+    "comm.cpp": [],
 }
+
+
+def _nccl():
+    """(include dir, lib dir) of the NCCL torch itself loads (the nvidia-nccl wheel), else the system's."""
+    try:
+        import nvidia.nccl as nn
+        base = os.path.dirname(nn.__file__) if nn.__file__ else list(nn.__path__)[0]
+        if os.path.exists(os.path.join(base, "include", "nccl.h")):
+            return os.path.join(base, "include"), os.path.join(base, "lib")
+    except ImportError:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 HEADERS = ["common.cuh", "internal.h"]
 
 
@@ -45,7 +58,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
             continue
         cmd = [NVCC] + ARCH + COMMON + extra + (["-Xptxas", "-v"] if ptxas_verbose else []) + ["-c", s, "-o", o]
         if src.endswith(".cpp"):
-            cmd = [NVCC] + COMMON + ["-x", "c++", "-c", s, "-o", o]
+            cmd = [NVCC] + COMMON + ["-I" + _nccl()[0], "-x", "c++", "-c", s, "-o", o]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,7 +68,9 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         if verbose and (r.stderr or r.stdout):
             print(r.stdout + r.stderr)
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        nlib = _nccl()[1]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-L" + nlib, "-l:libnccl.so.2",
+                                                              "-Xlinker", "-rpath=" + nlib]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

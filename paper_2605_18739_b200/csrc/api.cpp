@@ -919,6 +919,12 @@ kvq_status kvq_peer_pull_o(const kvq_peer* pe, int64_t epoch, void* O_shard, voi
   return cuda_status(launch_peer_pull_o(p, S(stream)));
 }
 
+kvq_status kvq_cache_get_config(const kvq_cache* c, kvq_config* out) {
+  if (!c || !out) return KVQ_EINVAL;
+  *out = c->cfg;
+  return KVQ_OK;
+}
+
 kvq_status kvq_debug_force_two_pass(kvq_cache* c, int32_t on) {
   if (!c) return KVQ_EINVAL;
   c->two_pass_only = on != 0;

@@ -108,6 +108,14 @@ _SIGS = {
     "kv_append_peer": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _P, _P]),
     "kvq_peer_signal_o": (ctypes.c_int, [_P, ctypes.c_int64, _P]),
     "kvq_peer_pull_o": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P]),
+    "kvq_cache_get_config": (ctypes.c_int, [_P, ctypes.POINTER(Config)]),
+    "kvq_get_unique_id": (ctypes.c_int, [_P]),
+    "kvq_comm_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)]),
+    "kvq_comm_destroy": (ctypes.c_int, [_P]),
+    "kvq_ulysses_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 6 + [ctypes.c_int, ctypes.c_int]),
+    "kvq_comm_configure": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t]),
+    "ulysses_chunk_attention": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, ctypes.c_int,
+                                               ctypes.POINTER(_Mask), ctypes.c_float, _P, ctypes.c_int, _P]),
     "kvq_debug_probe": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, _P]),
     "kvq_debug_set_trace": (ctypes.c_int, [_P]),
     "kvq_debug_force_two_pass": (ctypes.c_int, [_P, ctypes.c_int32]),
@@ -643,3 +651,65 @@ class Ulysses:
 
 def softmax_scale_default(d):
     return 1.0 / math.sqrt(d)
+
+
+EXCHANGE_INPUT, EXCHANGE_NVFP4, EXCHANGE_NVFP4_Q = 0, 1, 2
+
+
+class NcclUlysses:
+    """ulysses_chunk_attention with the library's own NCCL communicator (include/kvq.h, "One-call
+    head-sharded chunk step"; App. C, App. D).  The unique id is
+    made on rank 0 and broadcast over `group` (torch.distributed, any backend); after that every
+    collective of the step is issued by libkvq itself on the current stream."""
+
+    def __init__(self, cache: KVCache, H, rank, world, group=None, exchange=EXCHANGE_INPUT,
+                 in_dtype=torch.bfloat16, out_dtype=torch.bfloat16):
+        import torch.distributed as dist
+        L = lib()
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            _check(L.kvq_get_unique_id(buf), "kvq_get_unique_id")
+            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        if world > 1:
+            dev_uid = uid.to(cache.device) if dist.get_backend(group) == "nccl" else uid
+            dist.broadcast(dev_uid, 0, group=group)
+            uid = dev_uid.cpu()
+        raw = bytes(uid.numpy().tobytes())
+        h = ctypes.c_void_p()
+        _check(L.kvq_comm_create(ctypes.create_string_buffer(raw, 128), world, rank, ctypes.byref(h)),
+               "kvq_comm_create")
+        self._h = h
+        self.cache, self.H, self.P, self.rank = cache, H, world, rank
+        self.in_dtype, self.out_dtype = in_dtype, out_dtype
+        nb = int(L.kvq_ulysses_workspace_bytes(cache.T_c, H, cache.d, world, rank, exchange, _out_code(in_dtype),
+                                               _out_code(out_dtype)))
+        if nb == 0:
+            raise KVQError(-2, "kvq_ulysses_workspace_bytes")
+        self.ws = torch.empty(nb, dtype=torch.uint8, device=cache.device)
+        _check(L.kvq_comm_configure(self._h, H, exchange, _ptr(self.ws), nb), "kvq_comm_configure")
+
+    def step(self, layer, chunk_index, Q, K, V, mask: Mask, out=None, softmax_scale=0.0):
+        """Q, K, V: this rank's sequence shard [T_c/P, H, d] -> O shard [T_c/P, H, d] (out_dtype)."""
+        Ts = self.cache.T_c // self.P
+        for t in (Q, K, V):
+            if tuple(t.shape) != (Ts, self.H, self.cache.d) or t.dtype != self.in_dtype:
+                raise ValueError(f"expected [{Ts}, {self.H}, {self.cache.d}] {self.in_dtype}")
+        if out is None:
+            out = torch.empty((Ts, self.H, self.cache.d), dtype=self.out_dtype, device=Q.device)
+        m = mask._c()
+        _check(lib().ulysses_chunk_attention(self._h, self.cache._h, layer, chunk_index, _ptr(Q), _ptr(K), _ptr(V),
+                                             _dt(Q), ctypes.byref(m), softmax_scale, _ptr(out),
+                                             _out_code(self.out_dtype), _stream()), "ulysses_chunk_attention")
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _check(_lib.kvq_comm_destroy(self._h), "kvq_comm_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -33,7 +33,8 @@ def _declared():
 def test_header_declares_the_boundary():
     names = _declared()
     for n in ("kv_quantize_append", "chunk_attention", "kv_dequantize", "kv_export_chunk", "kvq_cache_create",
-              "kvq_ulysses_pack_qkv", "kvq_head_partition"):
+              "kvq_ulysses_pack_qkv", "kvq_head_partition", "ulysses_chunk_attention", "kvq_comm_create",
+              "kvq_get_unique_id"):
         assert n in names
     assert len(names) >= 22
 
@@ -88,3 +89,27 @@ def test_cache_bytes_and_validation(lib):
 def test_strerror(lib):
     assert lib.kvq_strerror(0) == b"ok"
     assert lib.kvq_strerror(-4).startswith(b"chunk")
+
+
+def test_native_ulysses_workspace_and_argument_checks(lib):
+    # host-only: workspace sizing and the synchronous argument errors (no NCCL call is reached)
+    T_c, H, d = 4680, 12, 128
+    b0 = lib.kvq_ulysses_workspace_bytes(T_c, H, d, 8, 0, 0, 0, 0)
+    b1 = lib.kvq_ulysses_workspace_bytes(T_c, H, d, 8, 0, 1, 0, 0)
+    b7 = lib.kvq_ulysses_workspace_bytes(T_c, H, d, 8, 7, 0, 0, 0)
+    Ts, act0 = T_c // 8, T_c * 2 * d * 2
+    # exchange 0 holds at least: send (the whole shard Q|K|V) + recv (3 x 2 heads x T_c) + local Q/K/V + O
+    assert b0 >= 3 * Ts * H * d * 2 + 3 * act0 + 3 * act0 + act0
+    assert b1 < b0 and b7 < b0  # NVFP4 K/V payload, and rank 7 owns one head instead of two
+    assert all(x % 256 == 0 for x in (b0, b1, b7))
+    assert lib.kvq_ulysses_workspace_bytes(T_c, H, d, 7, 0, 0, 0, 0) == 0  # T_c % P != 0
+    assert lib.kvq_ulysses_workspace_bytes(T_c, H, d, 8, 8, 0, 0, 0) == 0  # rank out of range
+    assert lib.kvq_ulysses_workspace_bytes(T_c, H, d, 8, 0, 3, 0, 0) == 0  # unknown exchange
+    out = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.kvq_comm_create(uid, 0, 0, ctypes.byref(out)) == -1
+    assert lib.kvq_comm_create(uid, 2, 2, ctypes.byref(out)) == -1
+    assert lib.kvq_comm_create(None, 1, 0, ctypes.byref(out)) == -1
+    assert lib.kvq_comm_destroy(None) == -1
+    assert lib.kvq_get_unique_id(None) == -1
+    assert lib.ulysses_chunk_attention(None, None, 0, 0, None, None, None, 0, None, 0.0, None, 0, None) == -1

@@ -332,3 +332,58 @@ def test_ulysses_nvfp4_exchange_wan_shape_p8():
         if ch == 2:
             O = torch.cat([O_locals[p] for p in range(P)], dim=1).cpu().numpy()   # [T, H, d] by head blocks
             check_fp32_out(O[rows], orc.attend(0, ch, q.f64, 3, 21, rows=rows))
+
+
+@pytest.mark.parametrize("exchange,io", [(0, "bf16"), (1, "bf16"), (2, "bf16"), (0, "fp32"), (1, "fp32")])
+def test_native_nccl_ulysses_world1(exchange, io):
+    # ulysses_chunk_attention: the whole head-sharded step behind one C call with libkvq's own NCCL
+    # communicator (one rank): O and the cache bytes equal the plain single-GPU path's
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d, H = 40, 3, 128, 12
+    T = tpf * fc
+    dt = torch.bfloat16 if io == "bf16" else torch.float32
+    mk = dict(sink_frames=3, window_frames=9, max_chunk_slots=8, device=DEV)
+    c_ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    c_nat = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    nat = kvq.NcclUlysses(c_nat, H, 0, 1, exchange=exchange, in_dtype=dt, out_dtype=dt)
+    try:
+        for ch in range(4):
+            q, k, v = synth.make_qkv(T, H, d, io, 0, ch)
+            Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+            mask = kvq.Mask(ch, 3, 9)
+            c_ref.append(0, ch, K, V)
+            O_ref = c_ref.attention(0, Q, mask, dt)
+            O = nat.step(0, ch, Q, K, V, mask)
+            torch.cuda.synchronize()
+            assert O.dtype == dt
+            if exchange == 2:  # NVFP4 Q: a different numerics mode (reading Z24), close to the plain one
+                assert torch.isfinite(O).all() and (O.float() - O_ref.float()).norm() < 0.2 * O_ref.float().norm()
+            else:
+                assert torch.equal(O, O_ref), (exchange, io, ch)
+            a, b = c_ref.export(0, ch), c_nat.export(0, ch)
+            assert all(torch.equal(a[n], b[n]) for n in a), (exchange, io, ch)
+    finally:
+        nat.close()
+
+
+def test_native_nccl_ulysses_argument_errors():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d, H = 40, 3, 128, 12
+    c = kvq.KVCache(1, H, d, tpf, fc, sink_frames=3, window_frames=9, max_chunk_slots=8, device=DEV, k_smoothing=True)
+    nat = kvq.NcclUlysses(c, H, 0, 1, exchange=kvq.EXCHANGE_INPUT)
+    try:
+        q, k, v = synth.make_qkv(tpf * fc, H, d, "bf16", 0, 0)
+        with pytest.raises(kvq.KVQError, match="EINVAL"):  # K-smoothing needs the NVFP4 exchange
+            nat.step(0, 0, q.torch(DEV), k.torch(DEV), v.torch(DEV), kvq.Mask(0, 3, 9))
+    finally:
+        nat.close()
+    c2 = kvq.KVCache(1, 5, d, tpf, fc, sink_frames=3, window_frames=9, max_chunk_slots=8, device=DEV)
+    nat2 = kvq.NcclUlysses(c2, H, 0, 1)
+    try:
+        q, k, v = synth.make_qkv(tpf * fc, H, d, "bf16", 0, 0)
+        with pytest.raises(kvq.KVQError, match="ESHAPE"):  # the cache must hold this rank's 12 heads
+            nat2.step(0, 0, q.torch(DEV), k.torch(DEV), v.torch(DEV), kvq.Mask(0, 3, 9))
+    finally:
+        nat2.close()
