@@ -42,6 +42,33 @@ __global__ void __launch_bounds__(512, 1) k(uint32_t* out, long long* cyc, int i
         asm volatile("prmt.b32 %0, %0, 0, 0x1044;" : "+r"(u[i]));
       } else if (OP == 7) {  // IMAD.U32 style shift (mul.lo by 65536)
         asm volatile("mul.lo.u32 %0, %0, 65536;" : "+r"(u[i]));
+      } else if (OP == 8) {  // attention softmax: F2FP.F16.F32.PACK_AB (+ LOP3 to consume it)
+        uint32_t r;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+        u[i] ^= r;
+      } else if (OP == 9) {  // MUFU.EX2
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+      } else if (OP == 10) {  // FHADD: fp32 += fp16 lane
+        asm volatile("{ .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.f16 %0, l, %0;\n}" : "+f"(a[i]) : "r"(u[i]));
+      } else if (OP == 11) {  // FMNMX3
+        asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(a[(i + 1) & 7]), "f"(a[(i + 2) & 7]));
+      } else if (OP == 12) {  // MUFU.EX2 + F2FP pack (shared pipe?)
+        float e;
+        uint32_t r;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a[i]));
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[(i + 3) & 7]), "f"(a[(i + 1) & 7]));
+        a[i] = e;
+        u[i] ^= r;
+      } else if (OP == 13) {  // MUFU.EX2 + FHADD
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+        float* b = reinterpret_cast<float*>(&x2[i]);
+        asm volatile("{ .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.f16 %0, l, %0;\n}" : "+f"(b[0]) : "r"(u[i]));
+      } else if (OP == 14) {  // F2FP pack + FHADD x2 (the P pack and the row sum per score pair)
+        uint32_t r;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+        float* b = reinterpret_cast<float*>(&x2[i]);
+        asm volatile("{ .reg .b16 l, h;\n mov.b32 {l, h}, %2;\n add.rn.f32.f16 %0, l, %0;\n add.rn.f32.f16 %1, h, %1;\n}"
+                     : "+f"(b[0]), "+f"(b[1]) : "r"(r));
       }
     }
   }
@@ -75,5 +102,12 @@ int main() {
   run<5>("F2FP.E4M3+LOP3", 1);
   run<6>("PRMT", 1);
   run<7>("IMUL 65536", 1);
+  run<8>("F2FP.F16.PACK+LOP3", 1);
+  run<9>("MUFU.EX2", 1);
+  run<10>("FHADD", 1);
+  run<11>("FMNMX3", 1);
+  run<12>("MUFU.EX2 + F2FP.F16", 1);
+  run<13>("MUFU.EX2 + FHADD", 1);
+  run<14>("F2FP.F16 + 2 FHADD", 1);
   return 0;
 }
