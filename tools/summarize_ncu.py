@@ -67,6 +67,38 @@ for rep, label in ((f"attn_{tag}", "attn_ws_kernel"), (f"quant_{tag}", "quant_sp
             return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(un, 1.0)
         traffic[label] = {"dram_read_MB": mb("dram__bytes_read.sum"), "dram_write_MB": mb("dram__bytes_write.sum"),
                           "bytes": (mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")) * 1e6, "source": rep}
+
+
+def stall_table(rep, region=None):
+    """Warp-stall sampling from the SASS source page: reasons summed over the kernel, and over a
+    SASS address range picked by `region` (first..last instruction whose text matches)."""
+    path = os.path.join(G, rep + ".ncu-rep")
+    if not os.path.exists(path):
+        return
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h = rows[1]
+    data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h)]
+    reasons = [x for x in h if x.startswith("stall_") and "Not Issued" not in x]
+    spans = [("whole kernel", 0, len(data) - 1)]
+    if region:
+        idx = [i for i, d in enumerate(data) if any(t in d["Source"] for t in region[1])]
+        if idx:
+            spans.append((region[0], idx[0], idx[-1]))
+    for label, lo, hi in spans:
+        tot = sum(float(data[i]["Warp Stall Sampling (All Samples)"] or 0) for i in range(lo, hi + 1))
+        agg = {r: sum(float(data[i][r] or 0) for i in range(lo, hi + 1)) for r in reasons}
+        top = sorted(agg.items(), key=lambda kv: -kv[1])[:8]
+        out.append(f"\n### {rep}: warp-stall samples, {label} ({int(tot)} samples)\n\n| reason | share |\n|---|---|\n")
+        for r, v in top:
+            out.append(f"| {r} | {100 * v / max(tot, 1):.1f}% |\n")
+
+
+stall_table(f"attn_{tag}", ("softmax max/exp/sum region (FMNMX3 .. FHADD)", ("FMNMX3", "MUFU.EX2", "FHADD")))
+stall_table(f"quant_{tag}")
+out.append("\n(Samples count every resident warp, including warps parked on mbarrier waits (BRA spin) "
+           "or at EXIT, so the whole-kernel shares mix roles; the region row isolates the softmax loop.)\n")
 open(os.path.join(P, f"ncu_summary_{tag}.md"), "w").write("".join(out))
 json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 os.system(f"cp {os.path.join(G, f'launches_{tag}.csv')} {os.path.join(P, f'launches_{tag}.csv')}")
