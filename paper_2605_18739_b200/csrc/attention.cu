@@ -37,8 +37,12 @@ namespace {
 
 constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant, MMA (+3 idle warps)
 // Register budget per SM sub-partition (16K regs = 4 warps x 128 at launch), rebalanced with
-// setmaxnreg: softmax 176 + 176, dequant 80, MMA warpgroup 80 (sum 512 per thread slot).
-constexpr int kRegSoftmax = 176, kRegDequant = 80, kRegMma = 80;
+// setmaxnreg: softmax 176 + 176, dequant 80, MMA warpgroup 80 (sum 512 per thread slot).  Swept
+// (tools/sweep_attn_flags.sh): 160 / 168 / 176 / 184 -> 858 / 843 / 839 / 923 us graph-timed; 176 kept.
+#ifndef KVQ_REG_SOFTMAX
+#define KVQ_REG_SOFTMAX 176
+#endif
+constexpr int kRegSoftmax = KVQ_REG_SOFTMAX, kRegDequant = 256 - KVQ_REG_SOFTMAX, kRegMma = 256 - KVQ_REG_SOFTMAX;
 // Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
 // FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
 #ifndef KVQ_POLY_PAIRS
