@@ -257,7 +257,14 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   p.mode = quant_mode(c);
   p.mean_out = c->cfg.k_smoothing ? mean_base(c, layer) + (size_t)slot * c->L.T_pad : nullptr;
   p.partials_w = partials;
-  // single pass when the chunk fits in aggregate shared memory, else amax pass + quantize pass
+  // amax supplied (no smoothing): the streaming quantize pass alone (10.7 us on the Wan chunk against
+  // 13.0 us for the single-pass kernel, which stages the whole chunk before quantizing).  Otherwise
+  // single pass when the chunk fits in aggregate shared memory, else amax pass + quantize pass.
+  if (ext_amax && !c->cfg.k_smoothing && !c->two_pass_only) {
+    if (launch_quantize2(p, sm_count(), st) != cudaSuccess) return KVQ_ECUDA;
+    commit_slot(c, layer, chunk, slot);
+    return KVQ_OK;
+  }
   cudaError_t e = c->two_pass_only ? cudaErrorNotSupported
                                    : launch_quantize_fused(p, reinterpret_cast<unsigned long long*>(c->arena + c->L.off_counters),
                                                            partials, sm_count(), st);

@@ -380,6 +380,26 @@ KVQ_DEV void unpack_block16(const uint8_t* src, float (&v)[16]) {  // generic po
   }
 }
 
+// the 16 values of one block from its raw 16-byte words (2 for bf16, 4 for fp32) in registers
+template <int DT>
+KVQ_DEV void unpack_raw16(const uint4 (&r)[DT == DT_BF16 ? 2 : 4], float (&v)[16]) {
+  if (DT == DT_BF16) {
+    const uint32_t w[8] = {r[0].x, r[0].y, r[0].z, r[0].w, r[1].x, r[1].y, r[1].z, r[1].w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[2 * k] = __uint_as_float(k < KVQ_UNPACK_PRMT ? bf16lo_prmt(w[k]) : w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 x = r[k];
+      v[4 * k] = __uint_as_float(x.x); v[4 * k + 1] = __uint_as_float(x.y);
+      v[4 * k + 2] = __uint_as_float(x.z); v[4 * k + 3] = __uint_as_float(x.w);
+    }
+  }
+}
+
 // Two-pass path, K with smoothing: per block (thread), row means by lane butterfly, written to the
 // head-major mean slot; per-CTA max |K_bar| into partials[0][blockIdx.x] (grid = kNumPartials).
 template <int DT, int D>
@@ -429,6 +449,9 @@ __global__ void __launch_bounds__(256) smooth_amax_kernel(const __grid_constant_
 // the decode scale and its reciprocal computed per block; blocks outside Markstein's range are
 // queued and redone with IEEE divisions.
 constexpr int kQ2Threads = 512;
+#ifndef KVQ_Q2_DEPTH
+#define KVQ_Q2_DEPTH 1  // quantize pass: iterations of input loaded ahead per thread (2 measured slower)
+#endif
 constexpr int kQ2NB = 2;  // blocks per thread per iteration
 
 template <int DT, int D, int MODE>
@@ -486,19 +509,44 @@ __global__ void __launch_bounds__(kQ2Threads, 1) quant2_kernel(const __grid_cons
     if (c == 0 && tid == 0) p.g_out[t] = g;
     uint8_t* codes = p.codes[t];
     uint8_t* scales = p.scales[t];
-    for (int i = tid; i < nu; i += kQ2NB * kQ2Threads) {
+    // the next iteration's input blocks are loaded into registers before this one is quantized, so
+    // each thread keeps a load in flight while it computes (the loop is otherwise latency-bound)
+    constexpr int kV4 = kUB / 16;  // 16-byte words per block
+    constexpr int kStep = kQ2NB * kQ2Threads;
+    uint4 raw[kQ2NB][kV4], raw2[kQ2NB][kV4];  // iterations i + kStep and (depth 2) i + 2 kStep
+    auto load_raw = [&](int i0, uint4 (&r)[kQ2NB][kV4]) {
+#pragma unroll
+      for (int b = 0; b < kQ2NB; ++b) {
+        const int ibb = i0 + b * kQ2Threads < nu ? i0 + b * kQ2Threads : i0;
+#pragma unroll
+        for (int w = 0; w < kV4; ++w) r[b][w] = __ldg(reinterpret_cast<const uint4*>(s + (size_t)ibb * kUB) + w);
+      }
+    };
+    if (tid < nu) load_raw(tid, raw);
+    if (KVQ_Q2_DEPTH > 1 && tid + kStep < nu) load_raw(tid + kStep, raw2);
+    for (int i = tid; i < nu; i += kStep) {
       int ib[kQ2NB];
       int64_t orow[kQ2NB];
 #pragma unroll
       for (int b = 0; b < kQ2NB; ++b) ib[b] = i + b * kQ2Threads < nu ? i + b * kQ2Threads : i;
       float v[kQ2NB][16];
 #pragma unroll
+      for (int b = 0; b < kQ2NB; ++b) unpack_raw16<DT>(raw[b], v[b]);
+      if (KVQ_Q2_DEPTH > 1) {
+#pragma unroll
+        for (int b = 0; b < kQ2NB; ++b)
+#pragma unroll
+          for (int w = 0; w < kV4; ++w) raw[b][w] = raw2[b][w];
+        if (i + 2 * kStep < nu) load_raw(i + 2 * kStep, raw2);
+      } else if (i + kStep < nu) {
+        load_raw(i + kStep, raw);
+      }
+#pragma unroll
       for (int b = 0; b < kQ2NB; ++b) {
         const uint32_t u = (uint32_t)u0 + (uint32_t)ib[b];  // 32-bit index math (rows * d/16 < 2^31)
         const uint32_t row = u / kNB;
         const uint32_t t_tok = div_small(row, (uint32_t)p.H, invH);
         orow[b] = (int64_t)(row - t_tok * (uint32_t)p.H) * p.head_stride_rows + t_tok;
-        unpack_block16<DT>(s + (size_t)ib[b] * kUB, v[b]);
         if (smooth_t) subtract_mean(v[b], p.mean_out[orow[b]]);
       }
       uint32_t sb[kQ2NB], w0[kQ2NB], w1[kQ2NB];

@@ -18,16 +18,21 @@ pool = [(torch.randn((T, H, d), generator=gen, device=dev).bfloat16(),
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
 
-def graph_time(n_app, cycle):
+amaxes = [torch.stack([k.float().abs().max(), v.float().abs().max()]).contiguous() for k, v in pool]
+
+
+def graph_time(n_app, cycle, ext=False):
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
+    kw = (lambda i: {"amax_kv": amaxes[i]}) if ext else (lambda i: {})
     with torch.cuda.stream(s):
-        c.append(0, 0, *pool[0])
+        c.append(0, 0, *pool[0], **kw(0))
     torch.cuda.current_stream().wait_stream(s)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for i in range(n_app):
-            c.append(0, 0, *pool[i % len(pool) if cycle else 0])
+            j = i % len(pool) if cycle else 0
+            c.append(0, 0, *pool[j], **kw(j))
     ts = []
     for _ in range(7):
         flush.zero_()
@@ -44,6 +49,11 @@ t_cold = graph_time(24, True)
 t_hot = graph_time(24, False)
 c.force_two_pass(True)
 t_two = graph_time(24, True)
+t_two_ext = graph_time(24, True, ext=True)
 c.force_two_pass(False)
+t_ext = graph_time(24, True, ext=True)
 print(f"append cold {t_cold:.2f} us ({BYTES / t_cold / 1e3:.0f} GB/s, {BYTES / t_cold / 1e3 / 6550.7:.1%} of 6550.7)"
       f" | L2-hot {t_hot:.2f} us | two-pass cold {t_two:.2f} us")
+print(f"amax supplied: kv_quantize_append_amax {t_ext:.2f} us ({BYTES / t_ext / 1e3:.0f} GB/s) | "
+      f"streaming quantize pass alone (forced) {t_two_ext:.2f} us ({BYTES / t_two_ext / 1e3:.0f} GB/s, "
+      f"{BYTES / t_two_ext / 1e3 / 6550.7:.1%})")
