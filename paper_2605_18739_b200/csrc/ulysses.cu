@@ -20,20 +20,31 @@ struct PackParams {
   int Ts, H, d, es, P;
 };
 
+// n / dv for n < 2^24 via a float reciprocal and one-step integer correction (exact)
+__device__ __forceinline__ uint32_t div_small_u(uint32_t n, uint32_t dv, float inv) {
+  uint32_t q = (uint32_t)__float2int_rz((float)n * inv);
+  if (q * dv > n) --q;
+  if ((q + 1) * dv <= n) ++q;
+  return q;
+}
+
+// 32-bit index math throughout (the launchers check byte offsets < 2^31 and rows < 2^24): 16-byte
+// chunks per row are a power of two (d * es / 16 in {8, 16, 32}), rows / H by div_small_u
 __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
-  const int cpr = p.d * p.es / 16;  // 16-byte chunks per (t, h) row
-  const int64_t per_tensor = (int64_t)p.Ts * p.H * cpr;
-  const int64_t total = 3 * per_tensor;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int tsr = (int)(i / per_tensor);
-    const int64_t rem = i - tsr * per_tensor;
-    const int64_t row = rem / cpr;
-    const int c = (int)(rem - row * cpr);
-    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+  const uint32_t cpr = (uint32_t)(p.d * p.es / 16), lc = (uint32_t)(__ffs((int)cpr) - 1);
+  const uint32_t per_tensor = (uint32_t)p.Ts * (uint32_t)p.H * cpr;
+  const uint32_t total = 3u * per_tensor;
+  const float invH = 1.0f / (float)p.H;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t tsr = i >= 2u * per_tensor ? 2u : (i >= per_tensor ? 1u : 0u);
+    const uint32_t rem = i - tsr * per_tensor;
+    const uint32_t row = rem >> lc, c = rem & (cpr - 1u);
+    const uint32_t t = div_small_u(row, (uint32_t)p.H, invH), h = row - t * (uint32_t)p.H;
     const int dst = p.owner[h];
     const int Hp = p.h0[dst + 1] - p.h0[dst];
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.x[tsr] + row * p.d * p.es) + c);
-    uint8_t* o = p.send + p.seg_off[dst] + (((int64_t)tsr * p.Ts + t) * Hp + (h - p.h0[dst])) * p.d * p.es;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.x[tsr] + (size_t)row * (p.d * p.es)) + c);
+    uint8_t* o = p.send + p.seg_off[dst] +
+                 (size_t)(((tsr * (uint32_t)p.Ts + t) * (uint32_t)Hp + (h - (uint32_t)p.h0[dst])) * (uint32_t)(p.d * p.es));
     reinterpret_cast<uint4*>(o)[c] = v;
   }
   if (blockIdx.x == 0) {  // amax of the local shard -> every destination's trailer
@@ -65,17 +76,14 @@ __global__ void __launch_bounds__(256) unpack_qkv_kernel(const uint8_t* recv, in
                                                          uint8_t* Q, uint8_t* K, uint8_t* V, float* amax_kv) {
   const int64_t blk = (int64_t)Ts * Hr * d * es;  // bytes of one tensor block from one source
   const int64_t seg = 3 * blk + 16;
-  const int64_t cpb = blk / 16;
-  const int64_t total = (int64_t)P * 3 * cpb;
-  uint8_t* outs[3] = {Q, K, V};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = i / cpb;  // (source, tensor) block
-    const int64_t c = i - b * cpb;
-    const int src = (int)(b / 3), tsr = (int)(b - (int64_t)src * 3);
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(recv + src * seg + tsr * blk) + c);
-    reinterpret_cast<uint4*>(outs[tsr] + src * blk)[c] = v;
-  }
-  if (blockIdx.x == 0 && threadIdx.x < 2) {  // global amax = max over every source's shard amax
+  const uint32_t cpb = (uint32_t)(blk / 16);
+  // blockIdx.y = (source, tensor) block: no index division at all
+  const int src = (int)blockIdx.y / 3, tsr = (int)blockIdx.y - 3 * src;
+  uint8_t* out = (tsr == 0 ? Q : (tsr == 1 ? K : V)) + src * blk;
+  const uint4* in = reinterpret_cast<const uint4*>(recv + src * seg + tsr * blk);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cpb; c += gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(out)[c] = __ldg(in + c);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) {  // global amax = max over every source's shard amax
     uint32_t m = 0;
     for (int src = 0; src < P; ++src) m = max(m, reinterpret_cast<const uint32_t*>(recv + src * seg + 3 * blk)[threadIdx.x]);
     amax_kv[threadIdx.x] = __uint_as_float(m);
@@ -92,17 +100,18 @@ struct UnpackOParams {
 };
 
 __global__ void __launch_bounds__(256) unpack_o_kernel(const __grid_constant__ UnpackOParams p) {
-  const int cpr = p.d * p.es / 16;
-  const int64_t total = (int64_t)p.Ts * p.H * cpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cpr;
-    const int c = (int)(i - row * cpr);
-    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+  const uint32_t cpr = (uint32_t)(p.d * p.es / 16), lc = (uint32_t)(__ffs((int)cpr) - 1);
+  const uint32_t total = (uint32_t)p.Ts * (uint32_t)p.H * cpr;
+  const float invH = 1.0f / (float)p.H;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t row = i >> lc, c = i & (cpr - 1u);
+    const uint32_t t = div_small_u(row, (uint32_t)p.H, invH), h = row - t * (uint32_t)p.H;
     const int src = p.owner[h];
     const int Hp = p.h0[src + 1] - p.h0[src];
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.recv + p.src_off[src] +
-                                                         ((int64_t)t * Hp + (h - p.h0[src])) * p.d * p.es) + c);
-    reinterpret_cast<uint4*>(p.out + row * p.d * p.es)[c] = v;
+                                                         (size_t)((t * (uint32_t)Hp + (h - (uint32_t)p.h0[src])) *
+                                                                  (uint32_t)(p.d * p.es))) + c);
+    reinterpret_cast<uint4*>(p.out + (size_t)row * (p.d * p.es))[c] = v;
   }
 }
 
@@ -292,6 +301,8 @@ cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int
   p.d = d;
   p.es = es;
   p.P = P;
+  // 32-bit index math in the kernel: every byte offset < 2^31, rows < 2^24
+  if (3 * (int64_t)Ts * H * d * es >= (1ll << 31) || (int64_t)Ts * H >= (1 << 24)) return cudaErrorInvalidValue;
   pack_kernel<<<grid_for(3 * (int64_t)Ts * H * d * es / 16), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
@@ -299,8 +310,13 @@ cudaError_t launch_ulysses_pack(const void* Q, const void* K, const void* V, int
 cudaError_t launch_ulysses_unpack_qkv(const uint8_t* recv, int dtype, int Ts, int Hr, int d, int P, void* Q, void* K,
                                       void* V, float* amax_kv, cudaStream_t st) {
   const int es = dtype == DT_FP32 ? 4 : 2;
-  unpack_qkv_kernel<<<grid_for((int64_t)P * 3 * Ts * Hr * d * es / 16), 256, 0, st>>>(
-      recv, Ts, Hr, d, es, P, (uint8_t*)Q, (uint8_t*)K, (uint8_t*)V, amax_kv);
+  const int64_t cpb = (int64_t)Ts * Hr * d * es / 16;
+  if (cpb >= (1ll << 31) || P > kMaxP) return cudaErrorInvalidValue;
+  int gx = (int)((cpb + 255) / 256);
+  const int cap = (148 * 8 + 3 * P - 1) / (3 * P);
+  gx = gx < 1 ? 1 : (gx > cap ? cap : gx);
+  unpack_qkv_kernel<<<dim3(gx, 3 * P), 256, 0, st>>>(recv, Ts, Hr, d, es, P, (uint8_t*)Q, (uint8_t*)K, (uint8_t*)V,
+                                                    amax_kv);
   return cudaGetLastError();
 }
 
@@ -322,6 +338,7 @@ cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int 
   p.d = d;
   p.es = es;
   p.P = P;
+  if ((int64_t)Ts * H * d * es >= (1ll << 31) || (int64_t)Ts * H >= (1 << 24)) return cudaErrorInvalidValue;
   unpack_o_kernel<<<grid_for((int64_t)Ts * H * d * es / 16), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
