@@ -133,53 +133,53 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
     }
     __syncthreads();
   }
-  const int64_t rows = (int64_t)p.Ts * p.Hr;      // per source
-  const int qc = p.d * p.es / 16, cc = p.d / 2 / 16;  // 16-byte chunks per Q row, per code row
-  const int64_t per_src = rows * (qc + 2 * cc);
-  const int64_t total = (int64_t)p.P * per_src;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int src = (int)(i / per_src);
-    int64_t r = i - src * per_src;
-    const uint8_t* seg = p.recv + src * p.seg;
+  // blockIdx.y = source; 32-bit index math within a source (chunks per Q / code row are powers of
+  // two, rows / Hr by div_small_u; the launcher checks rows < 2^24 and segment bytes < 2^31)
+  const uint32_t rows = (uint32_t)p.Ts * (uint32_t)p.Hr;  // per source
+  const uint32_t qc = (uint32_t)(p.d * p.es / 16), cc = (uint32_t)(p.d / 2 / 16);  // chunks per Q / code row
+  const uint32_t lq = (uint32_t)(__ffs((int)qc) - 1), lcc = (uint32_t)(__ffs((int)cc) - 1);
+  const uint32_t per_src = rows * (qc + 2 * cc);
+  const float invHr = 1.0f / (float)p.Hr;
+  const int src = (int)blockIdx.y;
+  const uint8_t* seg = p.recv + (int64_t)src * p.seg;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < per_src; r += gridDim.x * blockDim.x) {
     if (r < rows * qc) {  // Q chunk
-      const int64_t row = r / qc;
-      const int c = (int)(r - row * qc);
-      const int t = (int)(row / p.Hr), h = (int)(row - (int64_t)t * p.Hr);
+      const uint32_t row = r >> lq, c = r & (qc - 1u);
+      const uint32_t t = div_small_u(row, (uint32_t)p.Hr, invHr), h = row - t * (uint32_t)p.Hr;
       uint8_t* qdst = (uint8_t*)p.Q + (((int64_t)src * p.Ts + t) * p.Hr + h) * p.d * p.es;
       if (p.amax_q) {  // NVFP4 Q: 8 elements per 16-byte chunk of the fp16 row = dec(c) dec(s), exact
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(seg + p.lay.q + row * (p.d / 2) + c * 4);
-        const uint32_t sb = seg[p.lay.qs + row * (p.d / 16) + c / 2];
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(seg + p.lay.q + (size_t)row * (p.d / 2) + c * 4);
+        const uint32_t sb = seg[p.lay.qs + (size_t)row * (p.d / 16) + c / 2];
         uint32_t o[4];
         dequant_word_f16(w, f16x2_from_e4m3x2(sb | (sb << 8)), o);
         reinterpret_cast<uint4*>(qdst)[c] = make_uint4(o[0], o[1], o[2], o[3]);
       } else {
-        reinterpret_cast<uint4*>(qdst)[c] = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + row * p.d * p.es) + c);
+        reinterpret_cast<uint4*>(qdst)[c] = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + (size_t)row * p.d * p.es) + c);
       }
       continue;
     }
-    r -= rows * qc;
-    const int tsr = (int)(r / (rows * cc));
-    r -= (int64_t)tsr * rows * cc;
-    const int64_t row = r / cc;
-    const int c = (int)(r - row * cc);
-    const int t = (int)(row / p.Hr), h = (int)(row - (int64_t)t * p.Hr);
+    uint32_t k = r - rows * qc;
+    const int tsr = k >= rows * cc ? 1 : 0;
+    k -= (uint32_t)tsr * rows * cc;
+    const uint32_t row = k >> lcc, c = k & (cc - 1u);
+    const uint32_t t = div_small_u(row, (uint32_t)p.Hr, invHr), h = row - t * (uint32_t)p.Hr;
     const int64_t orow = (int64_t)h * p.head_stride_rows + (int64_t)src * p.Ts + t;
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + (tsr ? p.lay.vc : p.lay.kc) + row * (p.d / 2)) + c);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + (tsr ? p.lay.vc : p.lay.kc) + (size_t)row * (p.d / 2)) + c);
     reinterpret_cast<uint4*>(p.codes[tsr] + orow * (p.d / 2))[c] = v;
     if (c == 0) {  // the row's scale bytes (d/16) and K mean
-      const uint8_t* sc = seg + (tsr ? p.lay.vs : p.lay.ks) + row * (p.d / 16);
+      const uint8_t* sc = seg + (tsr ? p.lay.vs : p.lay.ks) + (size_t)row * (p.d / 16);
       uint8_t* dst = p.scales[tsr] + orow * (p.d / 16);
       if (p.d == 128) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(sc);
       else *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(sc);
       if (tsr == 0 && p.mean) p.mean[orow] = reinterpret_cast<const float*>(seg + p.lay.km)[row];
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 2 && p.amax_q) {  // g_Q for the attention's score scale
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 2 && p.amax_q) {  // g_Q for the score scale
     const uint32_t qb = __float_as_uint(p.amax_q[0]) & 0x7FFFFFFFu;
     if (qb >= 0x7F800000u) atomicCAS(&p.status->code, 0, -6);
     else *p.q_scale_out = qb == 0 ? 1.0f : __fdiv_rn(__uint_as_float(qb), 2688.0f);
   }
-  if (blockIdx.x == 0 && threadIdx.x < 2) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) {
     uint32_t mb = 0;
     if (!p.amax)  // f4: the mailbox (complete: the senders read it before storing)
       for (int r = 0; r < p.P; ++r) mb = max(mb, (uint32_t)p.mailbox[2 * r + threadIdx.x] & 0x7FFFFFFFu);
@@ -226,17 +226,17 @@ __global__ void __launch_bounds__(256) peer_pull_o_kernel(const __grid_constant_
     }
   }
   __syncthreads();
-  const int cpr = p.d * p.es / 16;
-  const int64_t total = (int64_t)p.Ts * p.H * cpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cpr;
-    const int c = (int)(i - row * cpr);
-    const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
+  const uint32_t cpr = (uint32_t)(p.d * p.es / 16), lc = (uint32_t)(__ffs((int)cpr) - 1);
+  const uint32_t total = (uint32_t)p.Ts * (uint32_t)p.H * cpr;
+  const float invH = 1.0f / (float)p.H;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t row = i >> lc, c = i & (cpr - 1u);
+    const uint32_t t = div_small_u(row, (uint32_t)p.H, invH), h = row - t * (uint32_t)p.H;
     const int r = p.owner[h];
     const int Hp = p.h0[r + 1] - p.h0[r];
     const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.o_src[r] + (((int64_t)p.rank * p.Ts + t) * Hp + (h - p.h0[r])) *
                                                                            p.d * p.es) + c);
-    reinterpret_cast<uint4*>(p.out + row * p.d * p.es)[c] = v;
+    reinterpret_cast<uint4*>(p.out + (size_t)row * (p.d * p.es))[c] = v;
   }
 }
 
@@ -268,13 +268,18 @@ cudaError_t launch_peer_signal(const PeerSignalParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_peer_pull_o(const PeerPullParams& p, cudaStream_t st) {
+  if ((int64_t)p.Ts * p.H * p.d * p.es >= (1ll << 31) || (int64_t)p.Ts * p.H >= (1 << 24)) return cudaErrorInvalidValue;
   peer_pull_o_kernel<<<grid_for((int64_t)p.Ts * p.H * (p.d * p.es / 16)), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st) {
-  const int64_t work = (int64_t)p.P * p.Ts * p.Hr * (p.d * p.es / 16 + p.d / 16);
-  scatter_nvfp4_kernel<<<grid_for(work), 256, 0, st>>>(p);
+  const int64_t per_src = (int64_t)p.Ts * p.Hr * (p.d * p.es / 16 + p.d / 16);
+  if ((int64_t)p.Ts * p.Hr >= (1 << 24) || per_src >= (1ll << 31) || p.P < 1) return cudaErrorInvalidValue;
+  int gx = (int)((per_src + 255) / 256);
+  const int cap = (148 * 8 + p.P - 1) / p.P;
+  gx = gx < 1 ? 1 : (gx > cap ? cap : gx);
+  scatter_nvfp4_kernel<<<dim3(gx, p.P), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 
