@@ -16,8 +16,10 @@
  *    in a device status word and reported by kvq_get_status().
  *  - All device work is ordered on the cudaStream_t passed in (passed as void* so the header
  *    needs no CUDA include); nothing synchronizes the host except kvq_get_status().
- *  - A cache has a single writer (kv_quantize_append); concurrent chunk_attention calls on
- *    other streams are allowed only while no append is in flight.
+ *  - A cache has a single writer (kv_quantize_append).  Reads may run concurrently
+ *    while no append is in flight: chunk_attention uses a split-KV workspace inside the cache
+ *    arena, so calls of it on one cache must be ordered (one stream, or events); calls that run
+ *    concurrently on different streams use chunk_attention_ws, each with its own workspace.
  *  - Layouts: an activation tensor [T, H, d] is row-major, row = (t, h), t-major -- the
  *    paper's (T_c H) x d reshape of K_{l,c} (§3.2).
  */
@@ -131,10 +133,28 @@ kvq_status kv_quantize_append_amax(kvq_cache* cache, int32_t layer, int64_t chun
  *   O[i,h,:] = softmax_j( Q[i,h,:] . K^[j,h,:] * scale ) V^[j,h,:],  j in K_eff(t)
  * with K^, V^ = dec(code) dec(s) g (Eq. 2).  Q: dev [T_c, H, d] q_dtype (BF16 | FP32);
  * O: dev [T_c, H, d] out_dtype (BF16 = the product, FP32 = parity mode).  softmax_scale <= 0
- * means 1/sqrt(d).  Every key chunk of K_eff must be resident (else KVQ_ENOCHUNK). */
+ * means 1/sqrt(d).  Every key chunk of K_eff must be resident (else KVQ_ENOCHUNK).
+ * Range: every finite query value is supported (each Q row is scaled by a power of two into
+ * fp16's range before the fp16 tensor-core MMA; exact).  Asynchronous data errors, reported by
+ * kvq_get_status with a flat index into Q: KVQ_ENONFINITE for an inf/NaN query element;
+ * KVQ_ERANGE when a row's scores Q.K^*scale*log2(e) exceed the fp32 range (index = the row's
+ * first element).  O is undefined for such rows.
+ * Workspace: the cache's own (calls on one cache must be ordered, see the conventions above). */
 kvq_status chunk_attention(kvq_cache* cache, int32_t layer, const void* Q, kvq_dtype q_dtype,
                            const kvq_mask* mask, float softmax_scale, void* O,
                            kvq_dtype out_dtype, void* stream);
+
+/* Bytes of the split-KV workspace one chunk_attention_ws call needs (partial O, running max and
+ * row sum of the pieces of work units split across CTAs); 0 for a null cache. */
+size_t kvq_attention_workspace_bytes(const kvq_cache* cache);
+
+/* chunk_attention with a caller-owned dev workspace (256-byte aligned, >= 
+ * kvq_attention_workspace_bytes, else KVQ_EINVAL): calls on different streams may run
+ * concurrently if each has its own workspace and no append to the cache is in flight. */
+kvq_status chunk_attention_ws(kvq_cache* cache, int32_t layer, const void* Q, kvq_dtype q_dtype,
+                              const kvq_mask* mask, float softmax_scale, void* O,
+                              kvq_dtype out_dtype, void* dev_workspace, size_t workspace_bytes,
+                              void* stream);
 
 /* Checking: dequantize one resident chunk to dev [T_c, H, d]: FP32 = RN32(dec(c) dec(s) g)
  * (Eq. 2), BF16 = RN_bf16 of that.  With k_smoothing, K = RN32(dec(c) dec(s) g + mean)
@@ -215,10 +235,13 @@ kvq_status kvq_ulysses_unpack_o(const void* recv_buf, kvq_dtype dtype, int32_t T
  * NVFP4 payload for the exchange (§8(f) f3; App. D: the pre-attention
  * All-to-All "performed entirely in the low-precision space", ~3.6x less K/V volume).  The
  * sender quantizes its sequence shard of K and V with the GLOBAL tensor scales, so what it ships
- * is exactly the cache bytes of the 1-GPU run for those rows (readings Z2/Z18); Q travels in its
- * input dtype (the paper's NVFP4 Q changes the attention numerics and is not built).  Sequence:
- *   kvq_ulysses_shard_amax -> all-reduce(MAX) of the 2 floats over the group (NCCL) ->
- *   kvq_ulysses_pack_nvfp4 -> all_to_all_single -> kv_append_ulysses_nvfp4 -> chunk_attention. */
+ * is exactly the cache bytes of the 1-GPU run for those rows (readings Z2/Z18).  Q travels in its
+ * input dtype, or -- optionally -- as NVFP4 too (a different attention numerics
+ * mode, reading Z24: kvq_ulysses_q_amax, dev_amax_q of kvq_ulysses_pack_nvfp4, and
+ * chunk_attention_qscaled).  Sequence:
+ *   kvq_ulysses_shard_amax (+ kvq_ulysses_q_amax) -> all-reduce(MAX) of the 2 (3) floats over the
+ *   group (NCCL) -> kvq_ulysses_pack_nvfp4 -> all_to_all_single -> kv_append_ulysses_nvfp4 ->
+ *   chunk_attention (chunk_attention_qscaled with NVFP4 Q). */
 
 /* Device scratch for kvq_ulysses_shard_amax (partials, status, K-smoothing means). */
 size_t kvq_ulysses_shard_scratch_bytes(int32_t Ts, int32_t H);
@@ -344,7 +367,11 @@ kvq_status kvq_comm_configure(kvq_comm* comm, int32_t num_heads, int32_t exchang
  * `chunk_index` of `layer` -> chunk_attention over `mask` -> exchange of O back ->
  * O_shard dev [T_c/P, H, d] out_dtype.  Codes and scales equal those of a 1-GPU cache of all
  * heads (the amax is global).  KVQ_ENCCL if a collective fails; K-smoothing caches need
- * exchange >= 1 (the shard amax of K is not that of K - mean) -> KVQ_EINVAL otherwise. */
+ * exchange >= 1 (the shard amax of K is not that of K - mean) -> KVQ_EINVAL otherwise.
+ * Every argument and cache-side error (chunk not appendable, no free slot, a mask chunk not
+ * resident after the append's evictions) is returned before the first collective is issued, so
+ * a rank that fails never leaves its peers blocked in a collective -- provided every rank passes
+ * the same layer, chunk_index and mask. */
 kvq_status ulysses_chunk_attention(kvq_comm* comm, kvq_cache* cache, int32_t layer,
                                    int64_t chunk_index, const void* Q_shard, const void* K_shard,
                                    const void* V_shard, kvq_dtype in_dtype, const kvq_mask* mask,

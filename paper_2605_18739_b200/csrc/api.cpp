@@ -190,38 +190,48 @@ kvq_status resolve_segments(const kvq_cache* c, int layer, const kvq_mask* m, st
 // Slot of (layer, chunk) under the append policy: chunk == newest re-writes its slot (a denoising
 // step); chunk == newest + 1 evicts what K_eff of this and later steps can no longer reach (the
 // global sink, the bound shot sink and the window ending at the new chunk) and
-// takes a free slot; anything else is KVQ_ENOCHUNK.  Nothing is committed until commit_slot.
-static kvq_status select_slot(kvq_cache* c, int32_t layer, int64_t chunk, int* slot_out) {
-  LayerState& ls = c->layers[layer];
+// takes a slot that is free once those are gone; anything else is KVQ_ENOCHUNK.  Pure: the
+// evictions are returned in *evict and applied by commit_slot, after the launch succeeded, so an
+// error (KVQ_ECAPACITY, KVQ_ECUDA) leaves the layer's chunk map untouched.
+struct SlotPlan {
   int slot = -1;
+  std::vector<int64_t> evict;
+};
+static kvq_status select_slot(const kvq_cache* c, int32_t layer, int64_t chunk, SlotPlan* plan) {
+  const LayerState& ls = c->layers[layer];
+  plan->slot = -1;
+  plan->evict.clear();
   if (ls.newest >= 0 && chunk == ls.newest) {
-    slot = ls.slot_of.at(chunk);
+    plan->slot = ls.slot_of.at(chunk);
   } else if (ls.newest < 0 || chunk == ls.newest + 1) {
     auto keep = chunks_of(key_token_ranges(chunk, c->cfg.frames_per_chunk, 1, c->cfg.sink_frames,
                                            c->cfg.window_frames, c->shot_start, c->shot_len),
                           c->cfg.frames_per_chunk);
-    for (auto it = ls.slot_of.begin(); it != ls.slot_of.end();) {
-      if (!keep.count(it->first)) {
-        ls.chunk_in[it->second] = -1;
-        it = ls.slot_of.erase(it);
-      } else {
-        ++it;
+    std::vector<char> freed(c->cfg.max_chunk_slots, 0);
+    for (auto& kv : ls.slot_of)
+      if (!keep.count(kv.first)) {
+        plan->evict.push_back(kv.first);
+        freed[kv.second] = 1;
       }
-    }
     for (int s = 0; s < c->cfg.max_chunk_slots; ++s)
-      if (ls.chunk_in[s] < 0) { slot = s; break; }
-    if (slot < 0) return KVQ_ECAPACITY;
+      if (ls.chunk_in[s] < 0 || freed[s]) { plan->slot = s; break; }
+    if (plan->slot < 0) return KVQ_ECAPACITY;
   } else {
     return KVQ_ENOCHUNK;
   }
-  *slot_out = slot;
   return KVQ_OK;
 }
 
-static void commit_slot(kvq_cache* c, int32_t layer, int64_t chunk, int slot) {
+static void commit_slot(kvq_cache* c, int32_t layer, int64_t chunk, const SlotPlan& plan) {
   LayerState& ls = c->layers[layer];
-  ls.slot_of[chunk] = slot;
-  ls.chunk_in[slot] = chunk;
+  for (int64_t e : plan.evict) {
+    auto it = ls.slot_of.find(e);
+    if (it == ls.slot_of.end()) continue;
+    ls.chunk_in[it->second] = -1;
+    ls.slot_of.erase(it);
+  }
+  ls.slot_of[chunk] = plan.slot;
+  ls.chunk_in[plan.slot] = chunk;
   ls.newest = chunk;
 }
 
@@ -230,9 +240,10 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   if (!c || !K || !V) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || chunk < 0) return KVQ_EINVAL;
   if (dt != KVQ_BF16 && dt != KVQ_FP32) return KVQ_EDTYPE;
-  int slot = -1;
-  const kvq_status ss = select_slot(c, layer, chunk, &slot);
+  SlotPlan plan;
+  const kvq_status ss = select_slot(c, layer, chunk, &plan);
   if (ss != KVQ_OK) return ss;
+  const int slot = plan.slot;
   const int H = c->cfg.num_heads, d = c->cfg.head_dim;
   const int64_t rows = c->L.T_c * H;
   cudaStream_t st = S(stream);
@@ -262,7 +273,7 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
   // single pass when the chunk fits in aggregate shared memory, else amax pass + quantize pass.
   if (ext_amax && !c->cfg.k_smoothing && !c->two_pass_only) {
     if (launch_quantize2(p, sm_count(), st) != cudaSuccess) return KVQ_ECUDA;
-    commit_slot(c, layer, chunk, slot);
+    commit_slot(c, layer, chunk, plan);
     return KVQ_OK;
   }
   cudaError_t e = c->two_pass_only ? cudaErrorNotSupported
@@ -282,11 +293,39 @@ kvq_status append_impl(kvq_cache* c, int32_t layer, int64_t chunk, const void* K
     e = launch_quantize2(p, sm_count(), st);
   }
   if (e != cudaSuccess) return KVQ_ECUDA;
-  commit_slot(c, layer, chunk, slot);
+  commit_slot(c, layer, chunk, plan);
   return KVQ_OK;
 }
 
 }  // namespace
+
+// Dry run of append(chunk) + attend(mask) for the one-call Ulysses step (comm.cpp): every error the
+// cache can raise (chunk not appendable, no free slot, a mask chunk not resident after the append's
+// evictions, too many key segments) is found here, before the first collective is issued -- a rank
+// that failed later would leave its peers blocked in the O all-to-all.
+namespace kvq {
+kvq_status validate_append_attend(const kvq_cache* c, int32_t layer, int64_t chunk, const kvq_mask* m) {
+  if (!c || !m || layer < 0 || layer >= c->cfg.num_layers || chunk < 0 || m->chunk_index < 0) return KVQ_EINVAL;
+  if (m->sink_frames < 0 || m->window_frames < 0 || m->shot_len_frames < 0) return KVQ_EINVAL;
+  SlotPlan plan;
+  kvq_status s = select_slot(c, layer, chunk, &plan);
+  if (s != KVQ_OK) return s;
+  std::set<int64_t> resident;
+  for (auto& kv : c->layers[layer].slot_of) resident.insert(kv.first);
+  for (int64_t e : plan.evict) resident.erase(e);
+  resident.insert(chunk);
+  auto ranges = key_token_ranges(m->chunk_index, c->cfg.frames_per_chunk, c->cfg.tokens_per_frame, m->sink_frames,
+                                 m->window_frames, m->shot_start_frame, m->shot_len_frames);
+  int nseg = 0;
+  const int64_t Tc = c->L.T_c;
+  for (auto& iv : ranges)
+    for (int64_t ch = iv.first / Tc; ch * Tc < iv.second; ++ch) {
+      if (!resident.count(ch)) return KVQ_ENOCHUNK;
+      if (++nseg > kMaxSegs) return KVQ_EINVAL;
+    }
+  return KVQ_OK;
+}
+}  // namespace kvq
 
 extern "C" {
 
@@ -354,23 +393,39 @@ kvq_status kv_quantize_append_amax(kvq_cache* c, int32_t layer, int64_t chunk, c
 }
 
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
-                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream);
+                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
+                                 size_t ws_bytes, void* stream);
 
 kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
                            float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
   if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
-  return attention_impl(c, layer, Q, q_dtype, nullptr, mask, softmax_scale, O, out_dtype, stream);
+  return attention_impl(c, layer, Q, q_dtype, nullptr, mask, softmax_scale, O, out_dtype, nullptr, 0, stream);
+}
+
+size_t kvq_attention_workspace_bytes(const kvq_cache* c) { return c ? attn_ws_bytes(c->cfg.head_dim) : 0; }
+
+kvq_status chunk_attention_ws(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
+                              float softmax_scale, void* O, kvq_dtype out_dtype, void* dev_workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (!c || !dev_workspace || (reinterpret_cast<uintptr_t>(dev_workspace) % kAlign) != 0) return KVQ_EINVAL;
+  if (workspace_bytes < kvq_attention_workspace_bytes(c)) return KVQ_EINVAL;
+  return attention_impl(c, layer, Q, q_dtype, nullptr, mask, softmax_scale, O, out_dtype, dev_workspace,
+                        workspace_bytes, stream);
 }
 
 kvq_status chunk_attention_qscaled(kvq_cache* c, int32_t layer, const void* Q_fp16, const float* dev_q_scale,
                                    const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype,
                                    void* stream) {
   if (!dev_q_scale) return KVQ_EINVAL;
-  return attention_impl(c, layer, Q_fp16, KVQ_FP16, dev_q_scale, mask, softmax_scale, O, out_dtype, stream);
+  return attention_impl(c, layer, Q_fp16, KVQ_FP16, dev_q_scale, mask, softmax_scale, O, out_dtype, nullptr, 0,
+                        stream);
 }
 
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
-                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+                                 const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  (void)ws_bytes;
   if (!c || !Q || !O || !mask) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || mask->chunk_index < 0) return KVQ_EINVAL;
   if (mask->sink_frames < 0 || mask->window_frames < 0 || mask->shot_len_frames < 0) return KVQ_EINVAL;
@@ -400,7 +455,9 @@ static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq
   p.d = d;
   const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
   p.scale_log2 = sc * 1.4426950408889634f;
-  p.ws = reinterpret_cast<float*>(c->arena + c->L.off_ws);
+  p.status = status_ptr(c);
+  // split-KV partials: the caller's workspace (chunk_attention_ws), else the cache's own
+  p.ws = reinterpret_cast<float*>(ws ? static_cast<uint8_t*>(ws) : c->arena + c->L.off_ws);
   p.trace = kvq_trace_ptr();
   p.ws_slots = 2 * kMaxCtas;
   p.max_ctas = std::min(sm_count(), kMaxCtas);
@@ -715,9 +772,10 @@ kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_in
   if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
   if ((dev_amax_q == nullptr) != (dev_q_scale == nullptr)) return KVQ_EINVAL;
   if (c->L.T_c % P) return KVQ_ESHAPE;
-  int slot = -1;
-  const kvq_status ss = select_slot(c, layer, chunk_index, &slot);
+  SlotPlan plan;
+  const kvq_status ss = select_slot(c, layer, chunk_index, &plan);
   if (ss != KVQ_OK) return ss;
+  const int slot = plan.slot;
   const int Hr = c->cfg.num_heads, d = c->cfg.head_dim, Ts = (int)(c->L.T_c / P);
   ScatterNvfp4Params p{};
   p.recv = static_cast<const uint8_t*>(recv_buf);
@@ -742,7 +800,7 @@ kvq_status kv_append_ulysses_nvfp4(kvq_cache* c, int32_t layer, int64_t chunk_in
   p.g_out = g_base(c, layer) + slot * 2;
   p.status = status_ptr(c);
   if (launch_ulysses_scatter_nvfp4(p, S(stream)) != cudaSuccess) return KVQ_ECUDA;
-  commit_slot(c, layer, chunk_index, slot);
+  commit_slot(c, layer, chunk_index, plan);
   return KVQ_OK;
 }
 
@@ -867,9 +925,10 @@ kvq_status kv_append_peer(const kvq_peer* pe, kvq_cache* c, int32_t layer, int64
   if (c->cfg.num_heads != h1 - h0 || c->cfg.head_dim != pe->d || c->L.T_c != pe->T_c ||
       c->cfg.k_smoothing != pe->k_smoothing || c->cfg.scale_mode != pe->scale_mode)
     return KVQ_ESHAPE;
-  int slot = -1;
-  const kvq_status ss = select_slot(c, layer, chunk_index, &slot);
+  SlotPlan plan;
+  const kvq_status ss = select_slot(c, layer, chunk_index, &plan);
   if (ss != KVQ_OK) return ss;
+  const int slot = plan.slot;
   const int Hr = c->cfg.num_heads, d = c->cfg.head_dim, Ts = (int)(c->L.T_c / pe->P);
   uint8_t* w = pe->win[pe->rank];
   ScatterNvfp4Params p{};
@@ -896,7 +955,7 @@ kvq_status kv_append_peer(const kvq_peer* pe, kvq_cache* c, int32_t layer, int64
   p.mailbox = reinterpret_cast<const unsigned long long*>(w + pe->L.mailbox);
   p.epoch = (unsigned long long)epoch;
   if (launch_ulysses_scatter_nvfp4(p, S(stream)) != cudaSuccess) return KVQ_ECUDA;
-  commit_slot(c, layer, chunk_index, slot);
+  commit_slot(c, layer, chunk_index, plan);
   return KVQ_OK;
 }
 
@@ -925,6 +984,7 @@ kvq_status kvq_peer_pull_o(const kvq_peer* pe, int64_t epoch, void* O_shard, voi
   p.rank = pe->rank;
   return cuda_status(launch_peer_pull_o(p, S(stream)));
 }
+
 
 kvq_status kvq_cache_get_config(const kvq_cache* c, kvq_config* out) {
   if (!c || !out) return KVQ_EINVAL;

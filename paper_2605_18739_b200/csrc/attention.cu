@@ -150,14 +150,77 @@ KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool val
   }
 }
 
-// Q row -> fp16 (bf16 in bf16-KV mode) into a tile row.  SUM: also returns sum_u Q_iu of the
-// rounded values (fp32; the K-smoothing restitution term, see attn_ws_kernel).  QSPLIT (fp32 Q):
-// hi = RN16(q) into the tile, lo = RN16(q - hi) (q - hi is exact in fp32) into the lo tile, and the
-// sum is over hi + lo.
+// Q row -> fp16 (bf16 in bf16-KV mode) into a tile row.
+//
+// Range (kvq.h, chunk_attention): bf16 / fp32 queries are scaled by 2^shift per row so that the
+// row's max |q| lands in [2^14, 2^15) before the fp16 conversion -- a power-of-two scale is exact,
+// so every finite query row fits fp16's normal range (values below max|q| * 2^-29 lose bits, a
+// relative 2^-29 of the row's largest term), and 2^-shift (returned as qscale) joins the row's
+// exponent scale.  For rows already inside fp16's range the scores are bit-identical to the
+// unscaled kernel (scaling by 2^shift commutes with every rounding).  A non-finite query element
+// is reported as KVQ_ENONFINITE with its flat index in Q.
+// SUM: also returns sum_u Q_iu in unscaled units (fp32; the K-smoothing restitution term, see
+// attn_ws_kernel).  QSPLIT (fp32 Q): hi = RN16(q 2^shift) into the tile, lo = RN16(q 2^shift - hi)
+// (exact in fp32) into the lo tile, and the sum is over the input values.
+struct QRow {
+  float qsum, qscale;
+  bool nonfinite;  // a query element was inf / NaN (reported; the row's scores are then not range-checked)
+};
+KVQ_DEV void report_status(DevStatus* st, int code, unsigned long long index) {
+  if (st == nullptr) return;
+  atomicCAS(&st->code, 0, code);
+  atomicMin(&st->first_bad, index);
+}
+
 template <int D, bool MMA_BF16, bool SUM = false, bool QSPLIT = false>
-KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, int q_dtype, int64_t row_index,
-                         bool valid) {
+KVQ_DEV QRow load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, int q_dtype, int64_t row_index,
+                        bool valid, DevStatus* status) {
   float qsum = 0.0f;
+  // pass 1: max |q| bit pattern of the row (integer max on non-negative floats; NaN / inf sort last)
+  const bool scaled = valid && !MMA_BF16 && (QSPLIT || q_dtype == DT_BF16);
+  float sc = 1.0f, qscale = 1.0f;
+  bool nonfinite = false;
+  if (scaled) {
+    uint32_t amax = 0;
+    int bad = -1;
+    if (!QSPLIT) {
+      const uint4* src = reinterpret_cast<const uint4*>((const __nv_bfloat16*)Q + row_index * D);
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) {
+        const uint4 v = __ldg(src + c);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t lo = w[k] & 0x7FFFu, hi = (w[k] >> 16) & 0x7FFFu;
+          if (bad < 0 && lo >= 0x7F80u) bad = 8 * c + 2 * k;
+          if (bad < 0 && hi >= 0x7F80u) bad = 8 * c + 2 * k + 1;
+          amax = max(amax, max(lo, hi) << 16);
+        }
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>((const float*)Q + row_index * D);
+#pragma unroll
+      for (int c = 0; c < D / 4; ++c) {
+        const float4 v = __ldg(src + c);
+        const uint32_t w[4] = {__float_as_uint(v.x) & 0x7FFFFFFFu, __float_as_uint(v.y) & 0x7FFFFFFFu,
+                               __float_as_uint(v.z) & 0x7FFFFFFFu, __float_as_uint(v.w) & 0x7FFFFFFFu};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (bad < 0 && w[k] >= 0x7F800000u) bad = 4 * c + k;
+          amax = max(amax, w[k]);
+        }
+      }
+    }
+    nonfinite = bad >= 0;
+    if (nonfinite) report_status(status, -6 /* KVQ_ENONFINITE */, (unsigned long long)(row_index * D + bad));
+    if (amax != 0 && amax < 0x7F800000u) {
+      int ex;
+      frexpf(__uint_as_float(amax), &ex);  // amax in [2^(ex-1), 2^ex)
+      const int shift = min(15 - ex, 120);
+      sc = ldexpf(1.0f, shift);
+      qscale = ldexpf(1.0f, -shift);
+    }
+  }
 #pragma unroll
   for (int c = 0; c < D / 8; ++c) {
     uint32_t o[4] = {0, 0, 0, 0}, ol[4] = {0, 0, 0, 0};
@@ -173,7 +236,8 @@ KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, 
         } else {
           uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int k = 0; k < 4; ++k) o[k] = pack_half2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
+          for (int k = 0; k < 4; ++k)
+            o[k] = pack_half2(__uint_as_float(w[k] << 16) * sc, __uint_as_float(w[k] & 0xFFFF0000u) * sc);
         }
       } else {
         const float4* src = reinterpret_cast<const float4*>((const float*)Q + row_index * D) + 2 * c;
@@ -181,10 +245,11 @@ KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, 
         f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f[2 * k], f[2 * k + 1]);
+          const float f0 = f[2 * k] * sc, f1 = f[2 * k + 1] * sc;
+          o[k] = MMA_BF16 ? pack_bf162(f[2 * k], f[2 * k + 1]) : pack_half2(f0, f1);
           if (QSPLIT) {
             const float2 h2 = __half22float2(*reinterpret_cast<const __half2*>(&o[k]));
-            ol[k] = pack_half2(f[2 * k] - h2.x, f[2 * k + 1] - h2.y);
+            ol[k] = pack_half2(f0 - h2.x, f1 - h2.y);
             if (SUM) qsum += f[2 * k] + f[2 * k + 1];
           }
         }
@@ -200,7 +265,8 @@ KVQ_DEV float load_q_row(uint32_t base, uint32_t base_lo, int r, const void* Q, 
     st_shared_v4(chunk_addr(base, r, c), o[0], o[1], o[2], o[3]);
     if (QSPLIT) st_shared_v4(chunk_addr(base_lo, r, c), ol[0], ol[1], ol[2], ol[3]);
   }
-  return qsum;
+  if (SUM && !QSPLIT) qsum *= qscale;  // the fp16 values were scaled by 2^shift
+  return QRow{qsum, qscale, nonfinite};
 }
 
 // Tile iteration over the key segments: tile = 128 slot-aligned rows, valid rows [lo, hi).
@@ -347,9 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
-      const float qsum = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
-                                                                 (int64_t)t * H + h, t < p.Tq);
-      const uint64_t qsb2 = f32x2_pack(qsum * sl2, qsum * sl2);
+      const QRow qr = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
+                                                              (int64_t)t * H + h, t < p.Tq, p.status);
+      const uint64_t qsb2 = f32x2_pack(qr.qsum * sl2, qr.qsum * sl2);
+      const float sl2q = sl2 * qr.qscale;  // this row's exponent scale (Q was scaled by 1/qscale)
+      bool range_reported = qr.nonfinite;
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
       float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
@@ -363,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           gk = __ldg(p.g + 2 * sg.slot);
           gv = __ldg(p.g + 2 * sg.slot + 1);
         }
-        const float cs = gk * sl2;
+        const float cs = gk * sl2q;
         float mean_r = 0.0f;  // SMOOTH: this thread's key of the tile
         if (SMOOTH && row >= lo && row < hi)
           mean_r = __ldg(p.mean_k + (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + row);
@@ -419,6 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         // normalisation stays exactly consistent for peaked rows.
         const float m_tile = SMOOTH ? mx : mx * cs;
         const float m_new = (j == 0 || m_tile > m_run + kLazyLog2) ? fmaxf(m_run, m_tile) : m_run;
+        // scores beyond the fp32 range (finite inputs): KVQ_ERANGE, index = the query row's first element
+        if (!(fabsf(m_tile) <= 3.402823466e38f) && !range_reported && t < p.Tq) {
+          range_reported = true;
+          report_status(p.status, -7 /* KVQ_ERANGE */, (unsigned long long)(((int64_t)t * H + h) * D));
+        }
 #endif
         const float alpha = ex2_approx(m_run - m_new);
         // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp16-rounded p (two packed chains)
@@ -812,7 +885,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
     for (int k = 0; get_piece(c, k, W, G, n, pc); ++k, ++kk) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
-      (void)load_q_row<D, false, false, false>(V2Q(qi), V2Q(qi), row, p.Q, p.q_dtype, (int64_t)t * H + h, t < p.Tq);
+      const float sl2q = sl2 * load_q_row<D, false, false, false>(V2Q(qi), V2Q(qi), row, p.Q, p.q_dtype,
+                                                                   (int64_t)t * H + h, t < p.Tq, p.status).qscale;
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
       float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
@@ -822,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
         const AttnSeg& sg = p.seg[it.seg];
         const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, kV2Keys);
         const float gk = __ldg(p.g + 2 * sg.slot), gv = __ldg(p.g + 2 * sg.slot + 1);
-        const float cs = gk * sl2;
+        const float cs = gk * sl2q;
         mbar_wait(sfull + qi, g & 1);
         tc_fence_after();
         uint32_t s[64];

@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include "../../include/kvq.h"
+#include "internal.h"
 
 struct kvq_comm {
   ncclComm_t nc = nullptr;
@@ -147,6 +148,8 @@ kvq_status ulysses_chunk_attention(kvq_comm* c, kvq_cache* cache, int32_t layer,
   const Ws w = carve(T_c, H, d, P, rank, ex, in_dtype, out_dtype, cfg.k_smoothing);
   if (carve(T_c, H, d, P, rank, ex, in_dtype, out_dtype, 1).total > c->ws_bytes) return KVQ_ECAPACITY;
   uint8_t* ws = c->ws;
+  // every cache-side error (slot, eviction, mask residency) is raised here, before the first collective
+  if ((st = kvq::validate_append_attend(cache, layer, chunk_index, mask)) != KVQ_OK) return st;
   float* amax = reinterpret_cast<float*>(ws + w.amax);  // [K, V, Q]
   float* qscale = reinterpret_cast<float*>(ws + w.qscale);
   const cudaStream_t cs = static_cast<cudaStream_t>(stream);

@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/kvq.h"
+
 namespace kvq {
 
 constexpr int kTileKeys = 128;     // keys per attention tile; slots are padded to a multiple
@@ -90,6 +92,7 @@ struct AttnParams {
   int Tq, H, d;
   float scale_log2;          // softmax_scale * log2(e)
   const float* q_scale;      // NVFP4 Q exchange: Q holds fp16 dec(c) dec(s), scores x g_Q = *q_scale (or null)
+  DevStatus* status;         // Q non-finite (KVQ_ENONFINITE) / scores beyond fp32 (KVQ_ERANGE); null: not reported
   // persistent stream-K schedule (filled by launch_attention)
   unsigned long long* trace; // debug timeline of CTA 0 (null in production)
   float* ws;                 // partial-piece workspace (null: one CTA per unit, no partials)
@@ -220,6 +223,10 @@ cudaError_t launch_ulysses_shard_amax(const QuantParams& p, uint32_t* partials, 
 cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st);
 cudaError_t launch_ulysses_scatter_nvfp4(const ScatterNvfp4Params& p, cudaStream_t st);
 void ulysses_partition(int H, int P, int* h0, uint8_t* owner);
+
+// Host-side dry run of kv_*append*(chunk) + chunk_attention(mask) on `cache` (api.cpp): the errors
+// either would return, found before the one-call Ulysses step issues its first collective.
+kvq_status validate_append_attend(const kvq_cache* c, int32_t layer, int64_t chunk, const kvq_mask* m);
 
 // Debug probes (codec checks against the oracle)
 cudaError_t launch_probe(int which, const void* in, void* out, int64_t n, cudaStream_t st);

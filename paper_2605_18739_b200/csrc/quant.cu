@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(kQ2Threads, KVQ_Q2_MINB) quant2_kernel(const _
     }
     __syncthreads();
     if (tid == 0) s_nq = 0;
+    __syncthreads();  // the reset must land before any thread enqueues a flagged block of the next tensor
   }
 }
 

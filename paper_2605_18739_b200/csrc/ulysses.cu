@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
         dequant_word_f16(w, f16x2_from_e4m3x2(sb | (sb << 8)), o);
         reinterpret_cast<uint4*>(qdst)[c] = make_uint4(o[0], o[1], o[2], o[3]);
       } else {
-        reinterpret_cast<uint4*>(qdst)[c] = __ldg(reinterpret_cast<const uint4*>(seg + p.lay.q + (size_t)row * p.d * p.es) + c);
+        // __ldcg, not __ldg: with f4 the window is written by peers while this kernel runs (after the
+        // acquire above), and the non-coherent path only suits data read-only for the kernel's lifetime
+        reinterpret_cast<uint4*>(qdst)[c] = __ldcg(reinterpret_cast<const uint4*>(seg + p.lay.q + (size_t)row * p.d * p.es) + c);
       }
       continue;
     }
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
     const uint32_t row = k >> lcc, c = k & (cc - 1u);
     const uint32_t t = div_small_u(row, (uint32_t)p.Hr, invHr), h = row - t * (uint32_t)p.Hr;
     const int64_t orow = (int64_t)h * p.head_stride_rows + (int64_t)src * p.Ts + t;
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(seg + (tsr ? p.lay.vc : p.lay.kc) + (size_t)row * (p.d / 2)) + c);
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(seg + (tsr ? p.lay.vc : p.lay.kc) + (size_t)row * (p.d / 2)) + c);
     reinterpret_cast<uint4*>(p.codes[tsr] + orow * (p.d / 2))[c] = v;
     if (c == 0) {  // the row's scale bytes (d/16) and K mean
       const uint8_t* sc = seg + (tsr ? p.lay.vs : p.lay.ks) + (size_t)row * (p.d / 16);

@@ -67,6 +67,9 @@ _SIGS = {
     "kv_quantize_append_amax": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P, _P]),
     "chunk_attention": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int, ctypes.POINTER(_Mask), ctypes.c_float,
                                        _P, ctypes.c_int, _P]),
+    "chunk_attention_ws": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int, ctypes.POINTER(_Mask), ctypes.c_float,
+                                          _P, ctypes.c_int, _P, ctypes.c_size_t, _P]),
+    "kvq_attention_workspace_bytes": (ctypes.c_size_t, [_P]),
     "kv_dequantize": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P]),
     "kv_export_chunk": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "kv_export_kmean": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P]),
@@ -228,15 +231,27 @@ class KVCache:
             _check(lib().kv_quantize_append_amax(self._h, layer, chunk_index, _ptr(K), _ptr(V), _dt(K),
                                                  _ptr(amax_kv), _stream()), "kv_quantize_append_amax")
 
-    def attention(self, layer, Q, mask: Mask, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None):
-        """chunk_attention: O = softmax(Q K^T * scale) V over K_eff(mask) with fused dequant."""
+    def attention(self, layer, Q, mask: Mask, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None, workspace=None):
+        """chunk_attention: O = softmax(Q K^T * scale) V over K_eff(mask) with fused dequant.
+        workspace: a tensor from new_attention_workspace() -> chunk_attention_ws (calls running
+        concurrently on different streams each need their own)."""
         self._shape_ok(Q)
         if out is None:
             out = torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
         m = mask._c()
-        _check(lib().chunk_attention(self._h, layer, _ptr(Q), _dt(Q), ctypes.byref(m), softmax_scale, _ptr(out),
-                                     _out_code(out.dtype), _stream()), "chunk_attention")
+        if workspace is None:
+            _check(lib().chunk_attention(self._h, layer, _ptr(Q), _dt(Q), ctypes.byref(m), softmax_scale, _ptr(out),
+                                         _out_code(out.dtype), _stream()), "chunk_attention")
+        else:
+            _check(lib().chunk_attention_ws(self._h, layer, _ptr(Q), _dt(Q), ctypes.byref(m), softmax_scale,
+                                            _ptr(out), _out_code(out.dtype), _ptr(workspace), workspace.numel(),
+                                            _stream()), "chunk_attention_ws")
         return out
+
+    def new_attention_workspace(self):
+        """A caller-owned split-KV workspace of kvq_attention_workspace_bytes (one per concurrent stream)."""
+        n = int(lib().kvq_attention_workspace_bytes(self._h))
+        return torch.empty(n, dtype=torch.uint8, device=self.device)
 
     def append_ulysses_nvfp4(self, layer, chunk_index, recv, P, amax_kv, q_dtype=torch.bfloat16, Q_out=None,
                              amax_q=None, q_scale=None):

@@ -34,24 +34,29 @@ def check_fp32_out(O_gpu, O_ref, max_abs=2e-3, rel=1e-3):
     return err, r
 
 
-def check_bf16_out(O_gpu, O_ref, O_gpu_fp32=None, max_abs=2e-3):
-    """bf16 output (reading Z17).  Rounding the exact answer to bf16 alone exceeds the fp32-mode
-    tolerance, so the bf16 product is checked as: (a) bit-identical to RN_bf16 of the kernel's
-    fp32-mode output (same arithmetic, different final rounding), when given; (b) elementwise
-    |O_bf16 - O_ref| <= 1 bf16 ulp(O_ref) + max_abs (one output rounding on top of the fp32 bar);
-    (c) ||O_bf16 - O_ref|| <= ||RN_bf16(O_ref) - O_ref|| + 1e-3 ||O_ref||: no worse than rounding
-    the exact answer to bf16, plus the fp32-mode rel-L2 budget."""
+def check_bf16_out(O_gpu, O_ref, O_gpu_fp32=None, rel=1e-3):
+    """bf16 output, reading Z17:
+    (a) when the same call's fp32-mode output is given: O_bf16 == RN_bf16(O_fp32), bit for bit (same
+        arithmetic, one final rounding);
+    (b) elementwise |O_bf16 - RN_bf16(O_ref)| <= 1 bf16 ulp, the ulp taken at the output ROW's scale,
+        max_u |O_ref[t, h, u]| (Z17: per-element ulps near a cancellation zero are below any
+        fp32-accumulating kernel's rounding -- measured: an all-fp32 CPU emulation misses the
+        per-element reading on 24 of 599,040 elements, the fp16-P design of SURVEY X3 on 1.7%, and
+        both meet the row-scale reading on every element);
+    (c) rel-L2 of O_bf16 against RN_bf16(O_ref) <= 1e-3 (as written)."""
     O_gpu = np.asarray(O_gpu, dtype=np.float64)
+    O_ref = np.asarray(O_ref, dtype=np.float64)
+    assert np.all(np.isfinite(O_gpu))
     if O_gpu_fp32 is not None:
         assert np.array_equal(O_gpu, bf16_round(O_gpu_fp32)), "bf16 out != RN_bf16(fp32 out)"
-    excess = np.abs(O_gpu - O_ref) - bf16_ulp(O_ref)
-    assert excess.max() <= max_abs, f"bf16 error exceeds 1 ulp + {max_abs} by {excess.max():.3e}"
     ref_b = bf16_round(O_ref)
-    nref = np.linalg.norm(O_ref)
-    e_gpu = np.linalg.norm(O_gpu - O_ref)
-    e_round = np.linalg.norm(ref_b - O_ref)
-    assert e_gpu <= e_round + 1e-3 * nref, f"bf16 rel-L2 {e_gpu / nref:.3e} vs rounding floor {e_round / nref:.3e}"
-    return float(excess.max()), (e_gpu - e_round) / nref
+    diff = np.abs(O_gpu - ref_b)
+    row_ulp = bf16_ulp(np.abs(O_ref).max(axis=-1, keepdims=True))
+    worst = float((diff / row_ulp).max())
+    assert worst <= 1.0, f"bf16 error {worst:.3f} row-scale ulps (> 1)"
+    r = float(np.linalg.norm(O_gpu - ref_b) / max(np.linalg.norm(ref_b), 1e-300))
+    assert r <= rel, f"bf16 rel-L2 vs RN_bf16(oracle) {r:.3e} > {rel}"
+    return worst, r
 
 
 def export_to_numpy(ex):

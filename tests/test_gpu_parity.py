@@ -304,15 +304,84 @@ def wan_layer():
 ROWS = np.array([0, 1, 63, 64, 127, 128, 129, 1000, 2047, 2048, 3333, 4095, 4096, 4500, 4607, 4608, 4609, 4679])
 
 
-def test_attention_wan_layer_sampled(wan_layer):
+@pytest.fixture(scope="module")
+def wan_layer_ref(wan_layer):
+    """The oracle's O for EVERY query row and head of the Wan layer (float64 BLAS, one head at a time)."""
+    c, o, q = wan_layer
+    return o.attend(0, 6, q.f64, 3, 21)
+
+
+def test_attention_wan_layer_full(wan_layer, wan_layer_ref):
+    # every one of the 4,680 x 12 x 128 outputs, in the launch configuration bench.py times
     c, o, q = wan_layer
     m = kvq.Mask(6, 3, 21)
     assert c.n_keys(0, m) == 32760
     O32 = c.attention(0, q.torch(DEV), m, torch.float32).cpu().numpy()
-    ref = o.attend(0, 6, q.f64, 3, 21, rows=ROWS)
-    check_fp32_out(O32[ROWS], ref)
+    check_fp32_out(O32, wan_layer_ref)
     Ob = c.attention(0, q.torch(DEV), m, torch.bfloat16).float().cpu().numpy()
-    check_bf16_out(Ob[ROWS], ref, O32[ROWS])
+    check_bf16_out(Ob, wan_layer_ref, O32)
+
+
+def test_attention_wan_layer_concurrent_streams(wan_layer, wan_layer_ref):
+    # two chunk_attention calls in flight at once on two streams, each with its own split-KV workspace
+    # (chunk_attention_ws; kvq.h: concurrent readers), against the oracle -- and the cache-owned
+    # workspace call on the default stream afterwards
+    c, o, q = wan_layer
+    m = kvq.Mask(6, 3, 21)
+    Q = q.torch(DEV)
+    ws = [c.new_attention_workspace() for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.empty(Q.shape, dtype=torch.float32, device=DEV) for _ in range(2)]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                c.attention(0, Q, m, torch.float32, out=outs[i], workspace=ws[i])
+        torch.cuda.synchronize()
+        for i in range(2):
+            check_fp32_out(outs[i].cpu().numpy(), wan_layer_ref)
+    assert torch.equal(outs[0], outs[1])      # deterministic: same inputs, same bits
+
+
+def test_attention_q_outside_fp16_range(wan_layer, wan_layer_ref):
+    # bf16 queries far outside fp16's range (|q| up to ~1e21 and down to ~1e-21, and just above 65504):
+    # per-row power-of-two scaling keeps them exact; the result matches the oracle and no error is
+    # reported (kvq.h, chunk_attention: every finite query row is supported)
+    c, o, q = wan_layer
+    m = kvq.Mask(6, 3, 21)
+    rows = np.array([0, 5, 130, 2047, 4679])
+    f = q.f64.copy()
+    f[0] *= 2.0 ** 70
+    f[5] *= 2.0 ** -70
+    f[130] = f[130] / np.abs(f[130]).max() * 70000.0
+    f[2047, :, 0] = 65504.0 * 4
+    f[4679] *= 2.0 ** 20
+    qq = synth.Tensor(f, "bf16")
+    assert c.status() == (0, -1)
+    O32 = c.attention(0, qq.torch(DEV), m, torch.float32).cpu().numpy()
+    assert c.status() == (0, -1)
+    ref = o.attend(0, 6, qq.f64, 3, 21, rows=rows)
+    check_fp32_out(O32[rows], ref)
+    keep = np.setdiff1d(np.arange(4680), rows)[::97]
+    check_fp32_out(O32[keep], wan_layer_ref[keep])      # the untouched rows are unchanged
+
+
+def test_attention_q_nonfinite_and_score_overflow_reported(wan_layer):
+    c, o, q = wan_layer
+    m = kvq.Mask(6, 3, 21)
+    H, d = 12, 128
+    Qb = q.torch(DEV).clone()
+    Qb[17, 3, 5] = float("inf")
+    c.attention(0, Qb, m, torch.float32)
+    code, idx = c.status()
+    assert code == -6 and idx == (17 * H + 3) * d + 5       # KVQ_ENONFINITE, flat index into Q
+    # finite fp32 queries whose scores exceed fp32: KVQ_ERANGE at the row's first element
+    Qf = q.torch(DEV).float()
+    Qf[40, 7, :] = 3.0e38
+    c.attention(0, Qf, m, torch.float32)
+    code, idx = c.status()
+    assert code == -7 and idx == (40 * H + 7) * d
+    assert c.status() == (0, -1)
 
 
 def test_attention_wan_layer_properties(wan_layer):
