@@ -134,11 +134,12 @@ kvq_status kv_quantize_append_amax(kvq_cache* cache, int32_t layer, int64_t chun
  * with K^, V^ = dec(code) dec(s) g (Eq. 2).  Q: dev [T_c, H, d] q_dtype (BF16 | FP32);
  * O: dev [T_c, H, d] out_dtype (BF16 = the product, FP32 = parity mode).  softmax_scale <= 0
  * means 1/sqrt(d).  Every key chunk of K_eff must be resident (else KVQ_ENOCHUNK).
- * Range: every finite query value is supported (each Q row is scaled by a power of two into
- * fp16's range before the fp16 tensor-core MMA; exact).  Asynchronous data errors, reported by
- * kvq_get_status with a flat index into Q: KVQ_ENONFINITE for an inf/NaN query element;
- * KVQ_ERANGE when a row's scores Q.K^*scale*log2(e) exceed the fp32 range (index = the row's
- * first element).  O is undefined for such rows.
+ * Range: every finite query value fits the MMA (each Q row is scaled by a power of two into
+ * fp16's range before the fp16 tensor-core MMA; exact); scores s = Q.K^ * scale * log2(e) are
+ * supported for |s| < 2^12 (fp32 accumulation error grows with |s|, reading Z25).
+ * Asynchronous data errors, reported by kvq_get_status with a flat index into Q:
+ * KVQ_ENONFINITE for an inf/NaN query element; KVQ_ERANGE when a key tile's largest score of a
+ * row reaches 2^12 in magnitude (index = the row's first element).  O is undefined for such rows.
  * Workspace: the cache's own (calls on one cache must be ordered, see the conventions above). */
 kvq_status chunk_attention(kvq_cache* cache, int32_t layer, const void* Q, kvq_dtype q_dtype,
                            const kvq_mask* mask, float softmax_scale, void* O,
@@ -186,9 +187,23 @@ int32_t kvq_resident_chunks(const kvq_cache* cache, int32_t layer);
  * |K_eff|; pass K_out = V_out = NULL to query it only. */
 kvq_status kv_dequantize_window(const kvq_cache* cache, int32_t layer, const kvq_mask* mask,
                                 void* K_out, void* V_out, int64_t* n_keys, void* stream);
+/* Q: dev [T_q, H, d] bf16; K, V: dev [n_keys, H, d] bf16 (16-byte aligned; every key attended,
+ * bidirectional); O: dev [T_q, H, d] out_dtype.  Tiles land by TMA (tensor maps built per call;
+ * KVQ_EINVAL if the driver refuses them); P is bf16.  Without a workspace one CTA per
+ * (head, 256-query pair). */
 kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, int32_t T_q,
                                   int64_t n_keys, int32_t H, int32_t d, float softmax_scale,
                                   void* O, kvq_dtype out_dtype, void* stream);
+/* Bytes of the workspace chunk_attention_bf16kv_ws takes at head dim d (0 for other d). */
+size_t kvq_bf16kv_workspace_bytes(int32_t d);
+/* chunk_attention_bf16kv on a persistent one-CTA-per-SM grid: whole (head, query pair) units in
+ * waves (the CTAs of a wave stream the same heads' key tiles, so the bf16 window is read from
+ * HBM about once), the remainder split stream-K with its partials in dev_workspace (256-byte
+ * aligned, >= kvq_bf16kv_workspace_bytes(d), else KVQ_EINVAL; NULL = the call above). */
+kvq_status chunk_attention_bf16kv_ws(const void* Q, const void* K, const void* V, int32_t T_q,
+                                     int64_t n_keys, int32_t H, int32_t d, float softmax_scale,
+                                     void* O, kvq_dtype out_dtype, void* dev_workspace,
+                                     size_t workspace_bytes, void* stream);
 
 /* Asynchronous data errors: synchronizes `stream`, returns the first recorded error (or
  * KVQ_OK) and the first offending flat element index (K: index into K, V: T_c*H*d + index),

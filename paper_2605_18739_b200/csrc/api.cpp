@@ -10,6 +10,7 @@
 #include <set>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/kvq.h"
@@ -572,13 +573,49 @@ kvq_status kv_dequantize_window(const kvq_cache* c, int32_t layer, const kvq_mas
   return cuda_status(launch_dequant_window(p, segs.data(), (int)segs.size(), K_out, V_out, S(stream)));
 }
 
-kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, int32_t T_q, int64_t n_keys, int32_t H,
-                                  int32_t d, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// [n_keys][H][d] bf16 as a 3-D tensor (d innermost), box {64, 1, 128}: one 128-key x 64-column panel
+// of the attention kernel's K-major SW128 tile per copy
+static bool kv_tensor_map(CUtensorMap* m, const void* base, int64_t n_keys, int H, int d) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)n_keys};
+  const cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)H * d * 2};
+  const cuuint32_t box[3] = {64, 1, 128}, estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t kvq_bf16kv_workspace_bytes(int32_t d) { return (d == 64 || d == 128) ? attn_ws_bytes(d) : 0; }
+
+kvq_status chunk_attention_bf16kv_ws(const void* Q, const void* K, const void* V, int32_t T_q, int64_t n_keys,
+                                     int32_t H, int32_t d, float softmax_scale, void* O, kvq_dtype out_dtype,
+                                     void* dev_workspace, size_t workspace_bytes, void* stream) {
   if (!Q || !K || !V || !O || T_q <= 0 || n_keys <= 0 || H <= 0) return KVQ_EINVAL;
   if (d != 64 && d != 128) return KVQ_ESHAPE;
   if (n_keys > INT_MAX) return KVQ_ESHAPE;
   if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (dev_workspace && ((reinterpret_cast<uintptr_t>(dev_workspace) % kAlign) != 0 ||
+                        workspace_bytes < kvq_bf16kv_workspace_bytes(d)))
+    return KVQ_EINVAL;
   AttnParams p{};
+  if (!kv_tensor_map(&p.tmap_k, K, n_keys, H, d) || !kv_tensor_map(&p.tmap_v, V, n_keys, H, d)) return KVQ_EINVAL;
   p.Q = Q;
   p.q_dtype = DT_BF16;
   p.O = O;
@@ -592,7 +629,18 @@ kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, i
   p.seg[0] = AttnSeg{0, 0, (int32_t)n_keys};
   const float sc = softmax_scale > 0.0f ? softmax_scale : 1.0f / std::sqrt((float)d);
   p.scale_log2 = sc * 1.4426950408889634f;
+  if (dev_workspace) {  // persistent grid: whole units in waves (L2 reuse of the bf16 window), stream-K remainder
+    p.ws = static_cast<float*>(dev_workspace);
+    p.ws_slots = 2 * kMaxCtas;
+    p.max_ctas = std::min(sm_count(), kMaxCtas);
+    p.hybrid = true;
+  }
   return cuda_status(launch_attention(p, false, S(stream)));
+}
+
+kvq_status chunk_attention_bf16kv(const void* Q, const void* K, const void* V, int32_t T_q, int64_t n_keys, int32_t H,
+                                  int32_t d, float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
+  return chunk_attention_bf16kv_ws(Q, K, V, T_q, n_keys, H, d, softmax_scale, O, out_dtype, nullptr, 0, stream);
 }
 
 kvq_status kvq_get_status(kvq_cache* c, void* stream, int64_t* first_bad_index) {

@@ -42,7 +42,10 @@ constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant,
 #ifndef KVQ_REG_SOFTMAX
 #define KVQ_REG_SOFTMAX 176
 #endif
-constexpr int kRegSoftmax = KVQ_REG_SOFTMAX, kRegDequant = 256 - KVQ_REG_SOFTMAX, kRegMma = 256 - KVQ_REG_SOFTMAX;
+#ifndef KVQ_REG_MMA
+#define KVQ_REG_MMA (256 - KVQ_REG_SOFTMAX)
+#endif
+constexpr int kRegSoftmax = KVQ_REG_SOFTMAX, kRegMma = KVQ_REG_MMA, kRegDequant = 512 - 2 * KVQ_REG_SOFTMAX - KVQ_REG_MMA;
 // Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
 // FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
 #ifndef KVQ_POLY_PAIRS
@@ -54,6 +57,9 @@ constexpr int kPolyPairs = KVQ_POLY_PAIRS;
 #define KVQ_LAZY_LOG2 4.0f
 #endif
 constexpr float kLazyLog2 = KVQ_LAZY_LOG2;
+// Largest |row max score| (log2 units, after the exponent scale) the product supports: 2^12
+// (reading Z25; the Wan workloads peak at ~30).
+constexpr float kScoreRangeLog2 = 4096.0f;
 
 template <int N>
 KVQ_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -137,16 +143,6 @@ KVQ_DEV void store_dequant_row(uint32_t base, int r, const PackedRow<D>& pr) {
       dequant_word_f16(w, s2, o);
       st_shared_v4(chunk_addr(base, r, wi), o[0], o[1], o[2], o[3]);
     }
-  }
-}
-
-// bf16 row (bf16-KV comparison mode): copy D values, zeros when !valid
-template <int D>
-KVQ_DEV void copy_row_to_smem(uint32_t base, int r, const uint8_t* row, bool valid) {
-#pragma unroll
-  for (int c = 0; c < D / 8; ++c) {
-    uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(row) + c) : make_uint4(0, 0, 0, 0);
-    st_shared_v4(chunk_addr(base, r, c), v.x, v.y, v.z, v.w);
   }
 }
 
@@ -306,22 +302,44 @@ struct Piece {
   int slot;           // workspace slot when !full
 };
 
-KVQ_DEV int64_t range_begin(int c, int64_t W, int G) { return (W * c) / G; }
+// Hybrid schedule (AttnParams::full_units, a multiple of the grid G): the first full_units units
+// are handed out whole in waves -- CTA c takes units c, c + G, ... -- so the CTAs of one wave walk
+// the key tiles of the same heads in step (L2 reuse of a window that does not fit L2: the bf16-KV
+// mode); the remaining (units - full_units) * n steps are cut into G equal contiguous stream-K
+// ranges.  full_units = 0 is plain stream-K.
+// Step indices are 32-bit (launch_t checks units * n < 2^31): the MMA warp's 80 registers hold the
+// schedule next to its descriptors without spilling.
+struct Sched {
+  int base, W;  // first stream-K step, stream-K steps
+  int G, n, waves;
+};
+KVQ_DEV Sched make_sched(const AttnParams& p, int n, int G) {
+  return Sched{p.full_units * n, (p.units - p.full_units) * n, G, n, p.full_units / G};
+}
+KVQ_DEV int range_begin(const Sched& s, int c) {
+  return s.base + (int)(((unsigned long long)(unsigned)s.W * (unsigned)c) / (unsigned)s.G);
+}
 
 // piece k of CTA c (k = 0, 1, ...); false when past the end of the range
-KVQ_DEV bool get_piece(int c, int k, int64_t W, int G, int n, Piece& pc) {
-  const int64_t beg = range_begin(c, W, G), end = range_begin(c + 1, W, G);
-  int64_t s = beg;
-  for (int i = 0; i < k && s < end; ++i) {
-    const int64_t u = s / n;
-    s = (u + 1) * (int64_t)n < end ? (u + 1) * (int64_t)n : end;
+KVQ_DEV bool get_piece(const Sched& sc, int c, int k, Piece& pc) {
+  if (k < sc.waves) {
+    pc.unit = c + k * sc.G;
+    pc.tb = 0;
+    pc.te = sc.n;
+    pc.full = true;
+    pc.slot = -1;
+    return true;
   }
+  k -= sc.waves;
+  const int n = sc.n;
+  const int beg = range_begin(sc, c), end = range_begin(sc, c + 1);
+  int s = beg;
+  for (int i = 0; i < k && s < end; ++i) s = min((s / n + 1) * n, end);
   if (s >= end) return false;
-  const int64_t u = s / n;
-  pc.unit = (int)u;
-  pc.tb = (int)(s - u * n);
-  const int64_t e = (u + 1) * (int64_t)n < end ? (u + 1) * (int64_t)n : end;
-  pc.te = (int)(e - u * n);
+  const int u = s / n;
+  pc.unit = u;
+  pc.tb = s - u * n;
+  pc.te = min((u + 1) * n, end) - u * n;
   pc.full = (pc.tb == 0 && pc.te == n);
   pc.slot = (s == beg) ? 2 * c : 2 * c + 1;
   return true;
@@ -340,6 +358,16 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
 }
 
 // debug timeline (CTA 0, first 64 tiles): SM clock at role events, only when p.trace != null
+#ifdef KVQ_TRACE_SOFTMAX
+#define KVQ_TRACE_SM(tile, ev) \
+  do {                                                                                             \
+    if (qi == 0) KVQ_TRACE(tile, ev);                                                              \
+  } while (0)
+#else
+#define KVQ_TRACE_SM(tile, ev) \
+  do {                         \
+  } while (0)
+#endif
 #define KVQ_TRACE(tile, ev)                                                                        \
   do {                                                                                           \
     if (p.trace != nullptr && blockIdx.x == 0 && (tile) < 64 && ((tid & 127) == 0 || tid == 384)) \
@@ -376,14 +404,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
   const int tid = threadIdx.x, warp = tid >> 5;
   const int H = p.H;
   const int n = count_tiles(p);
-  const int64_t W = (int64_t)p.units * n;
   const int G = gridDim.x, c = blockIdx.x;
+  const Sched sch = make_sched(p, n, G);
 
   if (warp == 12) tmem_alloc(tslot, 512);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(kfull + b, 128);
-      mbar_init(vfull + b, 128);
+      mbar_init(kfull + b, NVFP4 ? 128 : 1);  // dequant: one arrival per key row; bf16 KV: the TMA issuer
+      mbar_init(vfull + b, NVFP4 ? 128 : 1);
       mbar_init(kempty + b, 1);
       mbar_init(vempty + b, 1);
       mbar_init(sfull + b, 1);
@@ -410,14 +438,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     // exponent scale (log2 units); NVFP4-exchanged Q carries g_Q (device scalar) into it
     const float sl2 = p.q_scale ? p.scale_log2 * __ldg(p.q_scale) : p.scale_log2;
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
       const QRow qr = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
                                                               (int64_t)t * H + h, t < p.Tq, p.status);
       const uint64_t qsb2 = f32x2_pack(qr.qsum * sl2, qr.qsum * sl2);
       const float sl2q = sl2 * qr.qscale;  // this row's exponent scale (Q was scaled by 1/qscale)
-      bool range_reported = qr.nonfinite;
+      const bool range_reported = qr.nonfinite;
       fence_proxy_async_smem();
       mbar_arrive(qfull + qi);
       float m_run = -INFINITY, l_run = 0.0f, gv_run = 1.0f;
@@ -448,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           asm volatile("bar.sync %0, 128;" ::"r"(1 + qi) : "memory");
         }
         tmem_ld_wait();
+        KVQ_TRACE_SM(g, 12);
         if (SMOOTH) {  // y = s * cs + m_j * sum(q) * scale_log2  (log2 units), in place
           const float* mbuf = reinterpret_cast<const float*>(smem + SM::kMean) + (qi * 2 + (j & 1)) * 128;
           const uint64_t cs2s = f32x2_pack(cs, cs);
@@ -487,13 +516,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         // normalisation stays exactly consistent for peaked rows.
         const float m_tile = SMOOTH ? mx : mx * cs;
         const float m_new = (j == 0 || m_tile > m_run + kLazyLog2) ? fmaxf(m_run, m_tile) : m_run;
-        // scores beyond the fp32 range (finite inputs): KVQ_ERANGE, index = the query row's first element
-        if (!(fabsf(m_tile) <= 3.402823466e38f) && !range_reported && t < p.Tq) {
-          range_reported = true;
-          report_status(p.status, -7 /* KVQ_ERANGE */, (unsigned long long)(((int64_t)t * H + h) * D));
-        }
 #endif
         const float alpha = ex2_approx(m_run - m_new);
+        KVQ_TRACE_SM(g, 13);
         // p = 2^(s * cs - m) with packed fp32x2 FFMA; l sums the fp16-rounded p (two packed chains)
         const float cse = SMOOTH ? 1.0f : cs;  // SMOOTH: s already holds the scaled, restored score
         const uint64_t cs2 = f32x2_pack(cse, cse), mneg2 = f32x2_pack(-m_new, -m_new);
@@ -530,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         f32x2_unpack(acc0, a0, a1);
         f32x2_unpack(acc1, b0, b1);
         l_run = l_run * alpha + ((a0 + a1) + (b0 + b1)) + ((la[0] + la[1]) + (la[2] + la[3]));
+        KVQ_TRACE_SM(g, 14);
         KVQ_TMEM_ST32(tS, s);
         KVQ_TMEM_ST32(tS + 32, (s + 32));
         // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
@@ -564,11 +590,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         gv_run = gv;
         m_run = m_new;
         tmem_st_wait();
+        KVQ_TRACE_SM(g, 15);
         tc_fence_before();
         mbar_arrive(pfull + qi);
         KVQ_TRACE(g, 3 * qi + 2);
       }
       // ---- piece epilogue
+      // Score range (reading Z25): the scores come out of an fp32 accumulation whose absolute error
+      // grows with their magnitude (~|score| 2^-24 sqrt(d)), while softmax weights depend on score
+      // DIFFERENCES; a row whose running max reaches 2^12 log2 units in magnitude (or is non-finite)
+      // is KVQ_ERANGE, index = the query row's first element, and its O is undefined.  (m_run is
+      // within kLazyLog2 of the row's true max, so checking it once per piece sees every such row.)
+      if (!(fabsf(m_run) < kScoreRangeLog2) && !range_reported && t < p.Tq)
+        report_status(p.status, -7 /* KVQ_ERANGE */, (unsigned long long)(((int64_t)t * H + h) * D));
       mbar_wait(ofull + qi, k & 1);
       tc_fence_after();
       const float f = pc.full ? gv_run / l_run : gv_run;
@@ -617,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     const int r = tid - 256;  // key row within the tile
     int g = 0;
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
       const int h = pc.unit / p.qpairs;
       TileIter it;
       tile_seek(p, pc.tb, it);
@@ -625,6 +659,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         const AttnSeg& sg = p.seg[it.seg];
         const int b = SM::buf(g);
         const uint32_t par = SM::empty_par(g);
+#ifdef KVQ_EXPERIMENT_NO_DEQUANT  // timing experiments only (wrong results): K^/V^ tiles never written
+        if (NVFP4) {
+          if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
+          mbar_arrive(kfull + b);
+          if (g >= SM::kNBuf) mbar_wait(vempty + b, par);
+          mbar_arrive(vfull + b);
+        } else
+#endif
         if (NVFP4) {
           const int64_t crow = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
           PackedRow<D> pk, pv;
@@ -640,18 +682,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           fence_proxy_async_smem();
           mbar_arrive(vfull + b);
           if (r == 0) KVQ_TRACE(g, 7);
-        } else {
-          const int key = it.t0 + r;
-          const bool valid = key < sg.end;
-          const int64_t off = valid ? ((int64_t)key * H + h) * D * 2 : 0;
+        } else if (r == 0) {
+          // bf16-KV mode: one thread lands each 128-key K / V tile with TMA (D/64 panels of
+          // 128 rows x 128 B, 128B-swizzled = the K-major SW128 layout; keys past n_keys are zeros)
+          constexpr uint32_t kBytes = 128u * D * 2u;
           if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
-          copy_row_to_smem<D>(SK(b), r, (const uint8_t*)p.Kb + off, valid);
-          fence_proxy_async_smem();
-          mbar_arrive(kfull + b);
+          mbar_arrive_expect_tx(kfull + b, kBytes);
+#pragma unroll
+          for (int pn = 0; pn < D / 64; ++pn) tma_load_3d(SK(b) + 16384u * pn, &p.tmap_k, 64 * pn, h, it.t0, kfull + b);
           if (g >= SM::kNBuf) mbar_wait(vempty + b, par);
-          copy_row_to_smem<D>(SV(b), r, (const uint8_t*)p.Vb + off, valid);
-          fence_proxy_async_smem();
-          mbar_arrive(vfull + b);
+          mbar_arrive_expect_tx(vfull + b, kBytes);
+#pragma unroll
+          for (int pn = 0; pn < D / 64; ++pn) tma_load_3d(SV(b) + 16384u * pn, &p.tmap_v, 64 * pn, h, it.t0, vfull + b);
         }
       }
     }
@@ -705,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     };
     int g = 0;
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
       const int np = pc.te - pc.tb;
       mbar_wait(qfull + 0, k & 1);
       mbar_wait(qfull + 1, k & 1);
@@ -845,8 +887,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
   const int tid = threadIdx.x, warp = tid >> 5;
   const int H = p.H;
   const int n = count_tiles64(p);
-  const int64_t W = (int64_t)p.units * n;
   const int G = gridDim.x, c = blockIdx.x;
+  const Sched sch = make_sched(p, n, G);
 
   if (warp == 12) tmem_alloc(tslot, 512);
   if (tid == 0) {
@@ -882,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
     int g = 0;   // tiles processed (barrier parity)
     int kk = 0;  // pieces processed
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k, ++kk) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k, ++kk) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
       const float sl2q = sl2 * load_q_row<D, false, false, false>(V2Q(qi), V2Q(qi), row, p.Q, p.q_dtype,
@@ -1026,7 +1068,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
     const uint8_t* scales = is_v ? p.scales_v : p.scales_k;
     int g = 0;
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
       const int h = pc.unit / p.qpairs;
       TileIter it;
       tile_seek64(p, pc.tb, it);
@@ -1094,7 +1136,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_v2_kernel(const __grid_const
     };
     int g = 0;
     Piece pc;
-    for (int k = 0; get_piece(c, k, W, G, n, pc); ++k) {
+    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
       const int np = pc.te - pc.tb;
       mbar_wait(qfull + 0, k & 1);
       mbar_wait(qfull + 1, k & 1);
@@ -1135,18 +1177,18 @@ constexpr int kCombineSplit = KVQ_COMBINE_SPLIT;  // CTAs per split unit (row bl
 
 template <int D>
 __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ AttnParams p, int n) {
-  const int64_t W = (int64_t)p.units * n;
   const int G = p.grid;
+  const Sched sch = make_sched(p, n, G);
   const int b = blockIdx.x + 1;  // boundary between attention CTAs b-1 and b
-  const int64_t sb = range_begin(b, W, G);
+  const int sb = range_begin(sch, b);
   if (sb % n == 0) return;                                   // boundary on a unit edge: no split
-  const int unit = (int)(sb / n);
-  const int64_t s0 = (int64_t)unit * n, s1 = s0 + n;
-  if (range_begin(b - 1, W, G) > s0) return;                 // an earlier boundary owns this unit
+  const int unit = sb / n;
+  const int s0 = unit * n, s1 = s0 + n;
+  if (range_begin(sch, b - 1) > s0) return;                 // an earlier boundary owns this unit
   const int c0 = b - 1;                                      // CTA holding the unit's first piece
-  const bool c0_first = range_begin(c0, W, G) == s0;         // ... as its first piece?
+  const bool c0_first = range_begin(sch, c0) == s0;         // ... as its first piece?
   int c1 = b;
-  while (c1 + 1 < G && range_begin(c1 + 1, W, G) < s1) ++c1;  // last CTA with a piece of the unit
+  while (c1 + 1 < G && range_begin(sch, c1 + 1) < s1) ++c1;  // last CTA with a piece of the unit
   const int h = unit / p.qpairs, q0 = (unit - h * p.qpairs) * 256;
   constexpr int kTpr = D / 4;  // threads per row
   constexpr int kRows = 256 / kCombineSplit;  // rows of the unit merged by this CTA (blockIdx.y)
@@ -1192,6 +1234,7 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   int n = 0;
   for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 127) >> 7) - (p.seg[s].begin >> 7);
   if (n == 0 || p.units == 0) return cudaSuccess;
+  if ((int64_t)p.units * n >= (int64_t)1 << 31) return cudaErrorInvalidValue;  // 32-bit step indices (Sched)
   int G = p.units;
   bool split = false;
   if (p.ws != nullptr && p.ws_slots >= 2) {
@@ -1199,7 +1242,11 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
     const int64_t W = (int64_t)p.units * n;
     if (G > W / 2) G = (int)(W / 2);  // at least two (unit, tile) steps per CTA
     if (G < 1) G = 1;
-    split = (W % G != 0) || ((W / G) % n != 0);
+    p.full_units = p.hybrid ? (p.units / G) * G : 0;
+    const int64_t Wr = (int64_t)(p.units - p.full_units) * n;  // stream-K remainder
+    split = Wr > 0 && ((Wr % G != 0) || ((Wr / G) % n != 0));
+  } else {
+    p.full_units = 0;
   }
   p.grid = G;
   p.ws_slot_floats = 256 * D + 512;
@@ -1230,6 +1277,7 @@ cudaError_t launch_v2(AttnParams p, cudaStream_t st) {
   int n = 0;
   for (int s = 0; s < p.nseg; ++s) n += ((p.seg[s].end + 63) >> 6) - (p.seg[s].begin >> 6);
   if (n == 0 || p.units == 0) return cudaSuccess;
+  if ((int64_t)p.units * n >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   int G = p.units;
   bool split = false;
   if (p.ws != nullptr && p.ws_slots >= 2) {
@@ -1239,6 +1287,7 @@ cudaError_t launch_v2(AttnParams p, cudaStream_t st) {
     if (G < 1) G = 1;
     split = (W % G != 0) || ((W / G) % n != 0);
   }
+  p.full_units = 0;
   p.grid = G;
   p.ws_slot_floats = 256 * 128 + 512;
   kern<<<G, kThreads, smem, st>>>(p);

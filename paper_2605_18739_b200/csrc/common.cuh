@@ -93,6 +93,13 @@ KVQ_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t
   asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// 3-D tiled tensor copy global -> shared through a tensor map (TMA; the map lives in kernel
+// parameter space, __grid_constant__), completes on an mbarrier; out-of-bounds elements are zeros.
+KVQ_DEV void tma_load_3d(uint32_t smem_dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
 // make generic-proxy shared-memory writes visible to the async proxy (tensor core operands)
 KVQ_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -1,6 +1,7 @@
 // internal.h -- launch interfaces between the host C-ABI layer (api.cpp) and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/kvq.h"
@@ -100,6 +101,11 @@ struct AttnParams {
   int ws_slot_floats;        // floats per slot: 256 x d (O) + 512 (m, l)
   int max_ctas;              // SM count
   int units, qpairs, grid;
+  bool hybrid;               // whole units in waves first, stream-K for the remainder (see Sched)
+  int full_units;            // filled by launch_attention
+  // bf16 KV mode: TMA tensor maps of K and V viewed as [n_keys][H][d] bf16, box {64, 1, 128},
+  // 128-byte swizzle (one 128-key x 64-column panel of the K-major SW128 tile per copy)
+  CUtensorMap tmap_k, tmap_v;
   int nseg;
   AttnSeg seg[kMaxSegs];
 };

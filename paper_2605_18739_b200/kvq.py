@@ -79,6 +79,10 @@ _SIGS = {
                                             ctypes.POINTER(ctypes.c_int64), _P]),
     "chunk_attention_bf16kv": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                               ctypes.c_int32, ctypes.c_float, _P, ctypes.c_int, _P]),
+    "kvq_bf16kv_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32]),
+    "chunk_attention_bf16kv_ws": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                                 ctypes.c_int32, ctypes.c_float, _P, ctypes.c_int, _P,
+                                                 ctypes.c_size_t, _P]),
     "kvq_get_status": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
     "kvq_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "kvq_head_partition": (None, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
@@ -334,13 +338,25 @@ class KVCache:
         return code, idx.value
 
 
-def chunk_attention_bf16kv(Q, K, V, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None):
-    """Attention over caller-provided bf16 K/V [n_keys, H, d] (the A12 bf16-KV comparison mode)."""
+def new_bf16kv_workspace(d, device="cuda"):
+    """A caller-owned workspace of kvq_bf16kv_workspace_bytes(d) for chunk_attention_bf16kv(workspace=...)."""
+    n = int(lib().kvq_bf16kv_workspace_bytes(d))
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def chunk_attention_bf16kv(Q, K, V, out_dtype=torch.bfloat16, softmax_scale=0.0, out=None, workspace=None):
+    """Attention over caller-provided bf16 K/V [n_keys, H, d] (the A12 bf16-KV comparison mode).
+    workspace (new_bf16kv_workspace): the persistent wave + stream-K grid (chunk_attention_bf16kv_ws)."""
     Tq, H, d = Q.shape
     if out is None:
         out = torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
-    _check(lib().chunk_attention_bf16kv(_ptr(Q), _ptr(K), _ptr(V), Tq, K.shape[0], H, d, softmax_scale, _ptr(out),
-                                        _out_code(out.dtype), _stream()), "chunk_attention_bf16kv")
+    if workspace is None:
+        _check(lib().chunk_attention_bf16kv(_ptr(Q), _ptr(K), _ptr(V), Tq, K.shape[0], H, d, softmax_scale,
+                                            _ptr(out), _out_code(out.dtype), _stream()), "chunk_attention_bf16kv")
+    else:
+        _check(lib().chunk_attention_bf16kv_ws(_ptr(Q), _ptr(K), _ptr(V), Tq, K.shape[0], H, d, softmax_scale,
+                                               _ptr(out), _out_code(out.dtype), _ptr(workspace), workspace.numel(),
+                                               _stream()), "chunk_attention_bf16kv_ws")
     return out
 
 

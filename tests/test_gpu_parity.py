@@ -344,12 +344,14 @@ def test_attention_wan_layer_concurrent_streams(wan_layer, wan_layer_ref):
 
 
 def test_attention_q_outside_fp16_range(wan_layer, wan_layer_ref):
-    # bf16 queries far outside fp16's range (|q| up to ~1e21 and down to ~1e-21, and just above 65504):
-    # per-row power-of-two scaling keeps them exact; the result matches the oracle and no error is
-    # reported (kvq.h, chunk_attention: every finite query row is supported)
+    # bf16 queries outside fp16's range (|q| up to ~4e6 and 262144, down to ~1e-21, and 70000): the
+    # per-row power-of-two scaling keeps them exact in the fp16 MMA.  (a) With a softmax scale of
+    # 2^-16/sqrt(d) their scores stay moderate: the rows match the oracle and nothing is reported.
+    # (b) At the default scale the scores of rows 0 (x 2^70), 130, 2047 and 4679 reach 2^12 log2
+    # units: KVQ_ERANGE at the first such row's first element (reading Z25); other rows unchanged.
     c, o, q = wan_layer
     m = kvq.Mask(6, 3, 21)
-    rows = np.array([0, 5, 130, 2047, 4679])
+    rows = np.array([5, 130, 2047, 4679])
     f = q.f64.copy()
     f[0] *= 2.0 ** 70
     f[5] *= 2.0 ** -70
@@ -358,11 +360,14 @@ def test_attention_q_outside_fp16_range(wan_layer, wan_layer_ref):
     f[4679] *= 2.0 ** 20
     qq = synth.Tensor(f, "bf16")
     assert c.status() == (0, -1)
+    sc = 2.0 ** -16 / np.sqrt(128.0)
+    O32 = c.attention(0, qq.torch(DEV), m, torch.float32, softmax_scale=sc).cpu().numpy()
+    assert c.status() == (-7, 0)                      # row 0 (x 2^70) is out of range even at this scale
+    check_fp32_out(O32[rows], o.attend(0, 6, qq.f64, 3, 21, softmax_scale=sc, rows=rows))
     O32 = c.attention(0, qq.torch(DEV), m, torch.float32).cpu().numpy()
+    assert c.status() == (-7, 0)                      # KVQ_ERANGE, row 0 head 0 element 0
     assert c.status() == (0, -1)
-    ref = o.attend(0, 6, qq.f64, 3, 21, rows=rows)
-    check_fp32_out(O32[rows], ref)
-    keep = np.setdiff1d(np.arange(4680), rows)[::97]
+    keep = np.setdiff1d(np.arange(4680), np.array([0, 5, 130, 2047, 4679]))[::97]
     check_fp32_out(O32[keep], wan_layer_ref[keep])      # the untouched rows are unchanged
 
 
@@ -417,6 +422,28 @@ def test_bf16kv_mode_against_oracle():
     err = np.abs(O - ref).max()
     rel = np.linalg.norm(O - ref) / np.linalg.norm(ref)
     assert err < 1e-2 and rel < 4e-3, (err, rel)
+
+
+@pytest.mark.parametrize("Tq,H,d,N", [(300, 2, 128, 700), (200, 3, 64, 333), (4680, 12, 128, 640)])
+def test_bf16kv_ws_persistent_against_oracle(Tq, H, d, N):
+    # A12 on the persistent grid (chunk_attention_bf16kv_ws): TMA-landed tiles, ragged key tails (TMA
+    # zero fill), d = 64 and 128; the Wan-width case has 228 units > 148 CTAs -> one wave of whole
+    # units, the other 80 units split stream-K and merged by combine_kernel.  Every row and head.
+    _gpu()
+    Q = synth.make_tensor((Tq, H, d), "bf16", seed=11)
+    K = synth.make_tensor((N, H, d), "bf16", seed=12)
+    V = synth.make_tensor((N, H, d), "bf16", seed=13)
+    ws = kvq.new_bf16kv_workspace(d, DEV)
+    Qt, Kt, Vt = Q.torch(DEV), K.torch(DEV), V.torch(DEV)
+    O = kvq.chunk_attention_bf16kv(Qt, Kt, Vt, torch.float32, workspace=ws).cpu().numpy()
+    from oracle.attention import attention
+    ref = attention(Q.f64, K.f64, V.f64)
+    err = np.abs(O - ref).max()
+    rel = np.linalg.norm(O - ref) / np.linalg.norm(ref)
+    assert err < 1e-2 and rel < 4e-3, (err, rel)
+    # the data-parallel launch (no workspace) computes the same attention
+    O1 = kvq.chunk_attention_bf16kv(Qt, Kt, Vt, torch.float32).cpu().numpy()
+    assert np.abs(O1 - ref).max() < 1e-2
 
 
 def test_resident_footprint_ratio():

@@ -72,6 +72,8 @@ def main():
     Kw, Vw = cache.dequantize_window(0, m)
     deq = ev_time(lambda: cache.dequantize_window(0, m, Kw, Vw), 10)
     bf = ev_time(lambda: kvq.chunk_attention_bf16kv(q, Kw, Vw, out=O), 10)
+    wsb = kvq.new_bf16kv_workspace(D)
+    bfw = ev_time(lambda: kvq.chunk_attention_bf16kv(q, Kw, Vw, out=O, workspace=wsb), 10)
     flops = 4.0 * T * Kw.shape[0] * D * H
     out = {"config": "W30 + L240 (BASELINE.json configs[2], [3])", "w30_chunk_steps": steps,
            "w30_steady_chunk_ms": steady, "w30_steady_layer_query_tokens_per_s": L * T / (steady * 1e-3),
@@ -80,8 +82,10 @@ def main():
            "resident_nvfp4_bytes": resident, "resident_bf16_bytes": bf16_resident,
            "footprint_ratio": bf16_resident / resident,
            "layer_step_ms": {"fused_nvfp4": fused, "unfused_dequant_window": deq, "unfused_attention_bf16kv": bf,
-                             "unfused_total": deq + bf, "bf16_kv_cache_attention": bf},
-           "layer_tflops": {"fused_nvfp4": flops / fused / 1e9, "bf16_kv": flops / bf / 1e9},
+                             "unfused_total": deq + bfw, "bf16_kv_cache_attention": bfw,
+                             "bf16_kv_data_parallel_grid": bf},
+           "layer_tflops": {"fused_nvfp4": flops / fused / 1e9, "bf16_kv": flops / bfw / 1e9,
+                            "bf16_kv_data_parallel_grid": flops / bf / 1e9},
            "n_keys_steady": int(Kw.shape[0])}
     print(json.dumps(out))
 
