@@ -226,6 +226,20 @@ def rollout_w30(dev, steps=3):
     l240_s = (sum(ramp) + step_ms * (n_chunks - 7)) * 1e-3
     nv = cache.resident_bytes()
     bf16 = L * SLOTS * 2 * T_C * H * D * 2
+    # D4 throughput: one steady layer step's attention three ways (layer 0, chunk t_last resident):
+    # fused NVFP4 (the product), a bf16 KV cache (the same kernel family with TMA-landed bf16 tiles on
+    # the persistent grid, A12) and the paper's unfused design (dequantize the window to bf16, then A12)
+    m = kvq.Mask(t_last, SINK, WINDOW)
+    q = pool[(0 * 7 + t_last) % POOL][0]
+    Kw, Vw = cache.dequantize_window(0, m)
+    wsb = kvq.new_bf16kv_workspace(D)
+    fused = float(np.median([timed(lambda: cache.attention(0, q, m, out=O)) for _ in range(5)]))
+    bfkv = float(np.median([timed(lambda: kvq.chunk_attention_bf16kv(q, Kw, Vw, out=O, workspace=wsb)) for _ in range(5)]))
+    deq = float(np.median([timed(lambda: cache.dequantize_window(0, m, Kw, Vw)) for _ in range(5)]))
+    fl = 4.0 * T_C * Kw.shape[0] * D * H
+    cmp_ = {"n_keys": int(Kw.shape[0]), "fused_nvfp4_ms": fused, "bf16_kv_ms": bfkv, "unfused_dequant_ms": deq,
+            "unfused_total_ms": deq + bfkv, "fused_nvfp4_tflops": fl / fused / 1e9, "bf16_kv_tflops": fl / bfkv / 1e9,
+            "kv_bytes_per_layer_step": {"nvfp4": int(2 * Kw.shape[0] * H * D * 9 // 16), "bf16": int(2 * Kw.shape[0] * H * D * 2)}}
     return {"w30": {"config": "BASELINE.json configs[2]: 30 layers, sink 3 frames + window 21 frames, chunk t >= 7 "
                               "(37,440 keys per layer)",
                     "steady_chunk_step_ms": step_ms, "layer_query_tokens_per_s": L * T_C / (step_ms * 1e-3),
@@ -234,7 +248,7 @@ def rollout_w30(dev, steps=3):
             "l240": {"config": "BASELINE.json configs[3]: 320 chunks x 30 layers, one denoising pass",
                      "pass_s_extrapolated": l240_s, "extrapolation": "measured ramp steps t = 0..6 + 313 x the "
                      "measured steady chunk step", "resident_bytes_nvfp4": nv, "resident_bytes_bf16_kv": bf16,
-                     "footprint_ratio": bf16 / nv}}
+                     "footprint_ratio": bf16 / nv, "layer_step_nvfp4_vs_bf16_kv": cmp_}}
 
 
 
@@ -258,8 +272,12 @@ def run_gpu(args):
     Hr = h1 - h0
     nk = n_keys()
 
+    arena = None
+    if args.exchange == "peer" and (P > 1 or force):  # f4 direct: the owners' caches are written over peer memory
+        import torch.distributed._symmetric_memory as symm_mem
+        arena = symm_mem.empty(kvq.cache_bytes(1, Hr, D, TPF, T_FRAMES, SINK, WINDOW, 8), dtype=torch.uint8, device=dev)
     cache = kvq.KVCache(1, Hr, D, TPF, T_FRAMES, sink_frames=SINK, window_frames=WINDOW, max_chunk_slots=8,
-                        device=dev)
+                        device=dev, arena=arena)
     mask = kvq.Mask(CHUNK, SINK, WINDOW)
     Ts = T_C // P
     # synthetic chunk data (seeded); each rank holds its sequence shard of the full [T_c, H, d]

@@ -347,6 +347,36 @@ kvq_status kvq_peer_signal_o(const kvq_peer* peer, int64_t epoch, void* stream);
 /* O_shard dev [T_c/P, H, d] bf16. */
 kvq_status kvq_peer_pull_o(const kvq_peer* peer, int64_t epoch, void* O_shard, void* stream);
 
+/* f4 DIRECT (App. D): no staging copies at all.  The
+ * pack kernel stores each owner's NVFP4 rows straight into that owner's cache slot (and the
+ * bf16/fp32 Q rows into the owner's window), and the attention epilogue (and the split-KV
+ * combine) stores every O row straight into the O shard of the rank that owns its tokens.
+ * The cache arenas must be peer-accessible: `arenas` are the P ranks' kvq_cache arenas as seen
+ * from this rank (torch symmetric memory, or plain pointers for ranks simulated on one GPU);
+ * every rank's cache has the same config except num_heads = its head share, and all ranks
+ * make the same sequence of calls, so every rank's slot policy picks the same slot.
+ * Per step (epoch as above), on each rank's stream:
+ *   kvq_peer_publish_amax   (as above)
+ *   kv_append_peer_direct   waits (1-CTA kernel) for the mailbox, quantizes this rank's shard
+ *                           with the global scale into every owner's slot rows, then waits
+ *                           (1-CTA kernel) until all P sources stored into this rank's slot:
+ *                           on completion the local cache holds the chunk (and its g)
+ *   chunk_attention_peer    attention over the local heads, Q from the window, O rows into
+ *                           the owners' O shards over peer memory, then the O-ready signal
+ *   kvq_peer_wait_o         waits (1-CTA kernel) for all P signals; *O_shard = this rank's
+ *                           O shard [T_c/P, H, d] bf16 inside its window, valid until this
+ *                           rank's kvq_peer_publish_amax of epoch + 2.
+ * NVFP4 Q (reading Z24) is not offered on this path. */
+kvq_status kvq_peer_bind_caches(kvq_peer* peer, kvq_cache* cache, void* const* arenas);
+kvq_status kv_append_peer_direct(const kvq_peer* peer, int32_t layer, int64_t chunk_index,
+                                 const void* Q_shard, const void* K_shard, const void* V_shard,
+                                 int64_t epoch, void* stream);
+/* dev_workspace: NULL = the cache's own (see chunk_attention), else as chunk_attention_ws. */
+kvq_status chunk_attention_peer(const kvq_peer* peer, int32_t layer, const kvq_mask* mask,
+                                float softmax_scale, int64_t epoch, void* dev_workspace,
+                                size_t workspace_bytes, void* stream);
+kvq_status kvq_peer_wait_o(const kvq_peer* peer, int64_t epoch, void** O_shard, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * One-call head-sharded chunk step with a library-owned NCCL communicator (
  * PAPER.md:556-564 App. C, App. D).  Same kernels as the calls above, with

@@ -56,7 +56,8 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         objs.append(o)
         if not force and _mtime(o) > max(_mtime(s), hdr_time):
             continue
-        cmd = [NVCC] + ARCH + COMMON + extra + (["-Xptxas", "-v"] if ptxas_verbose else []) + ["-c", s, "-o", o]
+        dev_flags = os.environ.get("KVQ_NVCC_FLAGS", "").split()  # development A/B knobs (e.g. -DKVQ_QK_SPLIT=1)
+        cmd = [NVCC] + ARCH + COMMON + extra + dev_flags + (["-Xptxas", "-v"] if ptxas_verbose else []) + ["-c", s, "-o", o]
         if src.endswith(".cpp"):
             cmd = [NVCC] + COMMON + ["-I" + _nccl()[0], "-x", "c++", "-c", s, "-o", o]
         if verbose:

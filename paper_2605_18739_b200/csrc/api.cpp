@@ -393,9 +393,13 @@ kvq_status kv_quantize_append_amax(kvq_cache* c, int32_t layer, int64_t chunk, c
   return append_impl(c, layer, chunk, K, V, dt, dev_amax_kv, stream);
 }
 
+struct AttnRoute {  // f4 direct: O rows into the owning ranks' O shards (AttnParams::o_peer)
+  uint8_t* const* o_peer;
+  int P, Ts, H, h0;
+};
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
                                  const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
-                                 size_t ws_bytes, void* stream);
+                                 size_t ws_bytes, void* stream, const AttnRoute* route = nullptr);
 
 kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
                            float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
@@ -425,7 +429,7 @@ kvq_status chunk_attention_qscaled(kvq_cache* c, int32_t layer, const void* Q_fp
 
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
                                  const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
-                                 size_t ws_bytes, void* stream) {
+                                 size_t ws_bytes, void* stream, const AttnRoute* route) {
   (void)ws_bytes;
   if (!c || !Q || !O || !mask) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || mask->chunk_index < 0) return KVQ_EINVAL;
@@ -462,6 +466,12 @@ static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq
   p.trace = kvq_trace_ptr();
   p.ws_slots = 2 * kMaxCtas;
   p.max_ctas = std::min(sm_count(), kMaxCtas);
+  if (route) {
+    for (int r = 0; r < route->P; ++r) p.o_peer[r] = route->o_peer[r];
+    p.o_Ts = route->Ts;
+    p.o_H = route->H;
+    p.o_h0 = route->h0;
+  }
   return cuda_status(launch_attention(p, true, S(stream)));
 }
 
@@ -801,13 +811,13 @@ kvq_status kvq_ulysses_pack_nvfp4(const void* Q, const void* K, const void* V, k
   p.mode = (scale_mode == 1 ? kModeSearch : 0) | (k_smoothing ? kModeSmoothK : 0);
   p.amax = dev_amax_kv;
   p.amax_q = dev_amax_q;
-  p.send = static_cast<uint8_t*>(send_buf);
   ulysses_partition(H, P, p.h0, p.owner);
   int64_t off = 0;
   for (int r = 0; r < P; ++r) {
-    p.seg_off[r] = off;
-    p.lay[r] = nvfp4_seg_layout(Ts, p.h0[r + 1] - p.h0[r], d, (int)esize(dtype), k_smoothing != 0, dev_amax_q != nullptr);
-    off += p.lay[r].total;
+    const int Hp = p.h0[r + 1] - p.h0[r];
+    const Nvfp4SegLayout L = nvfp4_seg_layout(Ts, Hp, d, (int)esize(dtype), k_smoothing != 0, dev_amax_q != nullptr);
+    p.dst[r] = pack_dest_segment(static_cast<uint8_t*>(send_buf) + off, L, Hp);
+    off += L.total;
   }
   return cuda_status(launch_ulysses_pack_nvfp4(p, S(stream)));
 }
@@ -877,6 +887,11 @@ struct kvq_peer {
   kvq_dtype q_dtype;
   PeerWindowLayout L;
   uint8_t* win[kMaxP];
+  // f4 direct (kvq_peer_bind_caches): this rank's cache and every rank's cache arena + layout
+  kvq_cache* cache = nullptr;
+  uint8_t* arena[kMaxP];
+  Layout Lr[kMaxP];
+  int32_t h0[kMaxP + 1];
 };
 
 size_t kvq_peer_window_bytes(int32_t T_c, int32_t H, int32_t d, int32_t P, kvq_dtype q_dtype, int32_t k_smoothing) {
@@ -955,8 +970,9 @@ kvq_status kvq_peer_pack(const kvq_peer* pe, const void* Q, const void* K, const
   p.mode = (pe->scale_mode == 1 ? kModeSearch : 0) | (pe->k_smoothing ? kModeSmoothK : 0);
   ulysses_partition(pe->H, pe->P, p.h0, p.owner);
   for (int r = 0; r < pe->P; ++r) {
-    p.lay[r] = nvfp4_seg_layout(p.Ts, p.h0[r + 1] - p.h0[r], pe->d, (int)esize(pe->q_dtype), pe->k_smoothing != 0);
-    p.dst[r] = pe->win[r] + pe->L.recv + (int64_t)pe->rank * pe->L.seg;
+    const int Hp = p.h0[r + 1] - p.h0[r];
+    p.dst[r] = pack_dest_segment(pe->win[r] + pe->L.recv + (int64_t)pe->rank * pe->L.seg,
+                                 nvfp4_seg_layout(p.Ts, Hp, pe->d, (int)esize(pe->q_dtype), pe->k_smoothing != 0), Hp);
     p.arrive[r] = reinterpret_cast<unsigned long long*>(pe->win[r] + pe->L.arrive) + pe->rank;
   }
   p.mailbox = reinterpret_cast<const unsigned long long*>(pe->win[pe->rank] + pe->L.mailbox);
@@ -1033,6 +1049,127 @@ kvq_status kvq_peer_pull_o(const kvq_peer* pe, int64_t epoch, void* O_shard, voi
   return cuda_status(launch_peer_pull_o(p, S(stream)));
 }
 
+
+// ---- f4 direct: stores straight into the owners' cache slots and O shards
+kvq_status kvq_peer_bind_caches(kvq_peer* pe, kvq_cache* c, void* const* arenas) {
+  if (!pe || !c || !arenas) return KVQ_EINVAL;
+  int32_t a, b;
+  kvq_head_partition(pe->H, pe->P, pe->rank, &a, &b);
+  if (c->cfg.num_heads != b - a || c->cfg.head_dim != pe->d || c->L.T_c != pe->T_c ||
+      c->cfg.k_smoothing != pe->k_smoothing || c->cfg.scale_mode != pe->scale_mode)
+    return KVQ_ESHAPE;
+  if ((int64_t)pe->T_c * (b - a) * pe->d * (int64_t)esize(pe->q_dtype) > pe->L.mailbox) return KVQ_ESHAPE;  // Q_recv fits
+  for (int r = 0; r < pe->P; ++r) {
+    if (!arenas[r]) return KVQ_EINVAL;
+    kvq_head_partition(pe->H, pe->P, r, &pe->h0[r], &pe->h0[r + 1]);
+    kvq_config cr = c->cfg;
+    cr.num_heads = pe->h0[r + 1] - pe->h0[r];
+    pe->Lr[r] = make_layout(&cr);
+    pe->arena[r] = static_cast<uint8_t*>(arenas[r]);
+  }
+  // every kernel of the step is loaded now: under CUDA lazy loading a first launch could otherwise
+  // wait for in-flight work while a device-side wait (mailbox / arrivals / O flags) is pending
+  if (preload_peer_kernels() != cudaSuccess || preload_quant_kernels() != cudaSuccess ||
+      preload_attention_kernels() != cudaSuccess)
+    return KVQ_ECUDA;
+  pe->cache = c;
+  return KVQ_OK;
+}
+
+kvq_status kv_append_peer_direct(const kvq_peer* pe, int32_t layer, int64_t chunk_index, const void* Q, const void* K,
+                                 const void* V, int64_t epoch, void* stream) {
+  if (!pe || !pe->cache || !Q || !K || !V || epoch <= 0 || epoch >= (int64_t(1) << 32)) return KVQ_EINVAL;
+  kvq_cache* c = pe->cache;
+  if (layer < 0 || layer >= c->cfg.num_layers || chunk_index < 0) return KVQ_EINVAL;
+  SlotPlan plan;  // every rank runs the same policy on the same calls: the owners pick this slot too
+  const kvq_status ss = select_slot(c, layer, chunk_index, &plan);
+  if (ss != KVQ_OK) return ss;
+  const int slot = plan.slot, d = pe->d, Ts = pe->T_c / pe->P;
+  cudaStream_t st = S(stream);
+  uint8_t* w = pe->win[pe->rank];
+  PeerWaitParams wm{};  // every shard amax of this epoch is in the mailbox
+  wm.words = reinterpret_cast<const unsigned long long*>(w + pe->L.mailbox);
+  wm.n = 2 * pe->P;
+  wm.stride = 1;
+  wm.mode = 0;
+  wm.target = (unsigned long long)epoch;
+  if (launch_peer_wait(wm, st) != cudaSuccess) return KVQ_ECUDA;
+  PackNvfp4Params p{};
+  p.x[0] = Q;
+  p.x[1] = K;
+  p.x[2] = V;
+  p.dtype = pe->q_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32;
+  p.Ts = Ts;
+  p.H = pe->H;
+  p.d = d;
+  p.P = pe->P;
+  p.mode = quant_mode(c);
+  ulysses_partition(pe->H, pe->P, p.h0, p.owner);
+  const size_t es = esize(pe->q_dtype);
+  for (int r = 0; r < pe->P; ++r) {
+    const int Hp = pe->h0[r + 1] - pe->h0[r];
+    const Layout& Lr = pe->Lr[r];
+    const int64_t row0 = (int64_t)slot * Lr.T_pad + (int64_t)pe->rank * Ts;  // first row of this shard in the slot
+    const size_t lrows = (size_t)layer * Hp * Lr.rows_per_head;
+    PackDest& ds = p.dst[r];
+    ds.kc = pe->arena[r] + Lr.off_codes[0] + (lrows + row0) * (d / 2);
+    ds.vc = pe->arena[r] + Lr.off_codes[1] + (lrows + row0) * (d / 2);
+    ds.ks = pe->arena[r] + Lr.off_scales[0] + (lrows + row0) * (d / 16);
+    ds.vs = pe->arena[r] + Lr.off_scales[1] + (lrows + row0) * (d / 16);
+    ds.km = pe->k_smoothing ? reinterpret_cast<float*>(pe->arena[r] + Lr.off_mean) + lrows + row0 : nullptr;
+    ds.kv_ts = 1;
+    ds.kv_hs = Lr.rows_per_head;
+    ds.q = pe->win[r] + pe->L.recv + (size_t)pe->rank * Ts * Hp * d * es;  // owner's Q_recv [T_c, Hp, d]
+    ds.qs = nullptr;
+    ds.q_ts = Hp;
+    ds.q_hs = 1;
+    p.arrive[r] = reinterpret_cast<unsigned long long*>(pe->win[r] + pe->L.arrive) + pe->rank;
+  }
+  p.mailbox = reinterpret_cast<const unsigned long long*>(w + pe->L.mailbox);
+  p.epoch = (unsigned long long)epoch;
+  p.g_out = g_base(c, layer) + slot * 2;
+  p.status = status_ptr(c);
+  if (launch_ulysses_pack_nvfp4(p, st) != cudaSuccess) return KVQ_ECUDA;
+  PeerWaitParams wa{};  // every source's stores into this rank's slot and Q_recv have landed
+  wa.words = reinterpret_cast<const unsigned long long*>(w + pe->L.arrive);
+  wa.n = pe->P;
+  wa.stride = 1;
+  wa.mode = 1;
+  wa.target = (unsigned long long)epoch * (unsigned long long)ulysses_pack_grid(Ts, pe->H, d);
+  if (launch_peer_wait(wa, st) != cudaSuccess) return KVQ_ECUDA;
+  commit_slot(c, layer, chunk_index, plan);
+  return KVQ_OK;
+}
+
+kvq_status chunk_attention_peer(const kvq_peer* pe, int32_t layer, const kvq_mask* mask, float softmax_scale,
+                                int64_t epoch, void* dev_workspace, size_t workspace_bytes, void* stream) {
+  if (!pe || !pe->cache || !mask || epoch <= 0) return KVQ_EINVAL;
+  kvq_cache* c = pe->cache;
+  if (dev_workspace && ((reinterpret_cast<uintptr_t>(dev_workspace) % kAlign) != 0 ||
+                        workspace_bytes < kvq_attention_workspace_bytes(c)))
+    return KVQ_EINVAL;
+  uint8_t* o_peer[kMaxP];
+  for (int r = 0; r < pe->P; ++r) o_peer[r] = pe->win[r] + pe->L.o[epoch & 1];
+  const AttnRoute route{o_peer, pe->P, pe->T_c / pe->P, pe->H, pe->h0[pe->rank]};
+  const void* Qr = pe->win[pe->rank] + pe->L.recv;
+  const kvq_status s = attention_impl(c, layer, Qr, pe->q_dtype, nullptr, mask, softmax_scale, o_peer[pe->rank],
+                                      KVQ_BF16, dev_workspace, workspace_bytes, stream, &route);
+  if (s != KVQ_OK) return s;
+  return kvq_peer_signal_o(pe, epoch, stream);  // this rank's O rows (attention + combine) have landed
+}
+
+kvq_status kvq_peer_wait_o(const kvq_peer* pe, int64_t epoch, void** O_shard, void* stream) {
+  if (!pe || epoch <= 0) return KVQ_EINVAL;
+  PeerWaitParams wf{};
+  wf.words = reinterpret_cast<const unsigned long long*>(pe->win[pe->rank] + pe->L.flags);
+  wf.n = pe->P;
+  wf.stride = 1;
+  wf.mode = 2;
+  wf.target = (unsigned long long)epoch;
+  if (launch_peer_wait(wf, S(stream)) != cudaSuccess) return KVQ_ECUDA;
+  if (O_shard) *O_shard = pe->win[pe->rank] + pe->L.o[epoch & 1];
+  return KVQ_OK;
+}
 
 kvq_status kvq_cache_get_config(const kvq_cache* c, kvq_config* out) {
   if (!c || !out) return KVQ_EINVAL;

@@ -57,6 +57,23 @@ constexpr int kPolyPairs = KVQ_POLY_PAIRS;
 #define KVQ_LAZY_LOG2 4.0f
 #endif
 constexpr float kLazyLog2 = KVQ_LAZY_LOG2;
+// Split QK (build knob): S_i = [keys 0-63 | keys 64-127] as two N = 64 MMAs, P_i (fp16) stored in
+// the upper 64 columns; QK_i(j+1)'s first half is issued as soon as softmax_i(j) has loaded S_i(j)
+// into registers (the `sfree` barrier), so only its second half waits for PV_i(j) to consume P_i(j).
+#ifndef KVQ_QK_SPLIT
+#define KVQ_QK_SPLIT 0
+#endif
+constexpr bool kQkSplit = KVQ_QK_SPLIT != 0;
+// Store P of keys 0-63 to TMEM from inside the exponential loop (build knob), overlapping the
+// tcgen05.st with the second half of the loop (the MMA still waits for the whole tile's P).
+#ifndef KVQ_EARLY_STTM
+#define KVQ_EARLY_STTM 0
+#endif
+constexpr bool kEarlySttm = KVQ_EARLY_STTM != 0;
+// Row max as a 3-input max tree (build knob) instead of four dependent chains.
+#ifndef KVQ_MAX_TREE
+#define KVQ_MAX_TREE 0
+#endif
 // Largest |row max score| (log2 units, after the exponent scale) the product supports: 2^12
 // (reading Z25; the Wan workloads peak at ~30).
 constexpr float kScoreRangeLog2 = 4096.0f;
@@ -85,7 +102,7 @@ struct WsSmem {
   static constexpr int kQL1 = D == 128 ? 5 * kTile : 7 * kTile;
   static constexpr int kBar = (QSPLIT && D != 128) ? 8 * kTile : 6 * kTile;
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
-  static constexpr int kMean = kBar + 16 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
+  static constexpr int kMean = kBar + 18 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
   static constexpr int kBytes = kMean + 2 * 2 * 128 * 4 + 1024;
   // K^/V^ buffer of global tile g, and the mbarrier parities of its full / empty waits
   static KVQ_DEV int buf(int g) { return kNBuf == 2 ? (g & 1) : 0; }
@@ -399,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
   uint64_t* pfull = bars + 10;  // [2] softmax WG i -> MMA (P_i written, O_i rescaled)
   uint64_t* ofull = bars + 12;  // [2] MMA -> softmax WG i (last PV_i of a piece done)
   uint64_t* qfull = bars + 14;  // [2] softmax WG i -> MMA (Q_i tile of a piece loaded)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* sfree = bars + 16;  // [2] softmax WG i -> MMA (S_i loaded to registers; kQkSplit only)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int H = p.H;
@@ -418,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_init(pfull + b, 128);
       mbar_init(ofull + b, 1);
       mbar_init(qfull + b, 128);
+      mbar_init(sfree + b, 128);
     }
     fence_mbar_init();
   }
@@ -476,6 +495,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           asm volatile("bar.sync %0, 128;" ::"r"(1 + qi) : "memory");
         }
         tmem_ld_wait();
+        if (kQkSplit) {
+          tc_fence_before();
+          mbar_arrive(sfree + qi);  // S_i(j) is in registers: QK_i(j+1)'s first half may overwrite it
+        }
         KVQ_TRACE_SM(g, 12);
         if (SMOOTH) {  // y = s * cs + m_j * sum(q) * scale_log2  (log2 units), in place
           const float* mbuf = reinterpret_cast<const float*>(smem + SM::kMean) + (qi * 2 + (j & 1)) * 128;
@@ -497,6 +520,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           for (int kk = 0; kk < 128; ++kk)
             if (kk < lo || kk >= hi) s[kk] = __float_as_uint(-INFINITY);
         }
+#if KVQ_MAX_TREE
+        // 3-input max tree (depth 5: 128 -> 43 -> 15 -> 5 -> 2 -> 1), every level independent
+        float t43[43];
+#pragma unroll
+        for (int i = 0; i < 42; ++i)
+          t43[i] = fmax3(__uint_as_float(s[3 * i]), __uint_as_float(s[3 * i + 1]), __uint_as_float(s[3 * i + 2]));
+        t43[42] = fmaxf(__uint_as_float(s[126]), __uint_as_float(s[127]));
+        float t15[15];
+#pragma unroll
+        for (int i = 0; i < 14; ++i) t15[i] = fmax3(t43[3 * i], t43[3 * i + 1], t43[3 * i + 2]);
+        t15[14] = t43[42];
+        const float t5_0 = fmax3(t15[0], t15[1], t15[2]), t5_1 = fmax3(t15[3], t15[4], t15[5]),
+                    t5_2 = fmax3(t15[6], t15[7], t15[8]), t5_3 = fmax3(t15[9], t15[10], t15[11]),
+                    t5_4 = fmax3(t15[12], t15[13], t15[14]);
+        const float mx = fmaxf(fmax3(t5_0, t5_1, t5_2), fmaxf(t5_3, t5_4));
+#else
         // four independent 3-input max chains
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
@@ -507,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           mx3 = fmax3(mx3, __uint_as_float(s[kk + 6]), __uint_as_float(s[kk + 7]));
         }
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+#endif
 #ifdef KVQ_EXPERIMENT_NO_MAX  // timing experiments only (wrong results)
         const float m_new = j > 0 ? m_run : mx * cs;
 #else
@@ -537,14 +577,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           }
           const uint32_t pk = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
           s[kk] = pk;
+          if (kEarlySttm && kk == 31) KVQ_TMEM_ST32(tS + (kQkSplit ? 64 : 0), s);  // keys 0-63 final: store now
 #if defined(KVQ_SUM_UNROUNDED)
           if (kk & 1) acc1 = fadd2(acc1, f32x2_pack(p0, p1));
           else acc0 = fadd2(acc0, f32x2_pack(p0, p1));
 #elif !defined(KVQ_EXPERIMENT_NO_SUM)
           // mixed-precision adds (FHADD: fp32 += fp16 lane) of the rounded P, four chains
-          if (MMA_BF16) {
-            asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.bf16 %0, l, %0;\n add.rn.f32.bf16 %1, h, %1;\n}"
-                : "+f"(la[(kk & 1) * 2]), "+f"(la[(kk & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
+          if (MMA_BF16) {  // bf16 -> fp32 is exact bit placement (no native fp32 += bf16): FADD2 of the pair
+            const uint64_t r2 = f32x2_pack(__uint_as_float(pk << 16), __uint_as_float(pk & 0xFFFF0000u));
+            if (kk & 1) acc1 = fadd2(acc1, r2);
+            else acc0 = fadd2(acc0, r2);
           } else {
             asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.f16 %0, l, %0;\n add.rn.f32.f16 %1, h, %1;\n}"
                 : "+f"(la[(kk & 1) * 2]), "+f"(la[(kk & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
@@ -556,8 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         f32x2_unpack(acc1, b0, b1);
         l_run = l_run * alpha + ((a0 + a1) + (b0 + b1)) + ((la[0] + la[1]) + (la[2] + la[3]));
         KVQ_TRACE_SM(g, 14);
-        KVQ_TMEM_ST32(tS, s);
-        KVQ_TMEM_ST32(tS + 32, (s + 32));
+        if (!kEarlySttm) KVQ_TMEM_ST32(tS + (kQkSplit ? 64 : 0), s);
+        KVQ_TMEM_ST32(tS + (kQkSplit ? 96 : 32), (s + 32));
         // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
         // PV_i(j-1) is complete here (issued before QK_i(j), whose commit we waited on).
 #ifdef KVQ_EXPERIMENT_NO_RESCALE
@@ -634,6 +676,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
                                       __uint_as_float(o[4 * kk + 2]) * f, __uint_as_float(o[4 * kk + 3]) * f);
             } else {
               uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.O + base);
+              if (p.o_peer[0] != nullptr) {  // f4 direct: straight into the owning rank's O shard
+                const int r = t / p.o_Ts;
+                dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_peer[r]) +
+                                               ((int64_t)(t - r * p.o_Ts) * p.o_H + p.o_h0 + h) * D + 32 * cc);
+              }
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
                 dst[kk] = make_uint4(pack_bf162(__uint_as_float(o[8 * kk]) * f, __uint_as_float(o[8 * kk + 1]) * f),
@@ -683,13 +730,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           mbar_arrive(vfull + b);
           if (r == 0) KVQ_TRACE(g, 7);
         } else if (r == 0) {
-          // bf16-KV mode: one thread lands each 128-key K / V tile with TMA (D/64 panels of
-          // 128 rows x 128 B, 128B-swizzled = the K-major SW128 layout; keys past n_keys are zeros)
+          // bf16-KV mode: one thread (warp 8) lands each 128-key K tile with TMA, another (warp 9)
+          // each V tile, so neither stream waits on the other's buffer (D/64 panels of 128 rows x
+          // 128 B, 128B-swizzled = the K-major SW128 layout; keys past n_keys are zeros)
           constexpr uint32_t kBytes = 128u * D * 2u;
           if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
           mbar_arrive_expect_tx(kfull + b, kBytes);
 #pragma unroll
           for (int pn = 0; pn < D / 64; ++pn) tma_load_3d(SK(b) + 16384u * pn, &p.tmap_k, 64 * pn, h, it.t0, kfull + b);
+        } else if (r == 32) {
+          constexpr uint32_t kBytes = 128u * D * 2u;
           if (g >= SM::kNBuf) mbar_wait(vempty + b, par);
           mbar_arrive_expect_tx(vfull + b, kBytes);
 #pragma unroll
@@ -706,6 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     // lane issues each unrolled group of tcgen05.mma and its commits.  Descriptor bases are
     // precomputed; the k-step offsets are compile-time adds to the start-address field.
     constexpr uint32_t kIdS = umma_idesc_f16(128, 128, MMA_BF16 ? 1 : 0, 0, 0);
+    constexpr uint32_t kIdS64 = umma_idesc_f16(128, 64, MMA_BF16 ? 1 : 0, 0, 0);
     constexpr uint32_t kIdO = umma_idesc_f16(128, D, MMA_BF16 ? 1 : 0, 0, 1);
     const uint64_t dQ0 = umma_desc_sw128(SQ(0), 16, 1024), dQ1 = umma_desc_sw128(SQ(1), 16, 1024);
     const uint64_t dL0 = umma_desc_sw128(SQL(0), 16, 1024), dL1 = umma_desc_sw128(SQL(1), 16, 1024);
@@ -731,9 +782,30 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       }
       __syncwarp();
     };
+    // kQkSplit: keys [64 half, 64 half + 64) of the tile into S_i columns [64 half, +64)
+    auto issue_qk_half = [&](int qi, int b, int half) {
+      const uint64_t da = qi ? dQ1 : dQ0, db = (b ? dK1 : dK0) + (uint64_t)((8192 * half) >> 4);
+      const uint32_t dt = tmem + 128u * qi + 64u * half;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+          umma_ss(dt, da + off, db + off, kIdS64, kk > 0 ? 1u : 0u);
+        }
+        if (QSPLIT) {
+          const uint64_t dl = qi ? dL1 : dL0;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+            umma_ss(dt, dl + off, db + off, kIdS64, 1u);
+          }
+        }
+      }
+      __syncwarp();
+    };
     auto issue_pv = [&](int qi, int b, bool first) {
       const uint64_t db = b ? dV1 : dV0;
-      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + 128u * qi;
+      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + 128u * qi + (kQkSplit ? 64u : 0u);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -760,27 +832,43 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       tc_commit(kempty + SM::buf(g));
       for (int j = 0; j < np; ++j) {
         const int gj = g + j, b = SM::buf(gj), bn = SM::buf(gj + 1);
+        const bool more = j + 1 < np;
+        if (kQkSplit && more) {  // QK_0(j+1), keys 0-63, while softmax_0(j) runs
+          mbar_wait(kfull + bn, SM::full_par(gj + 1));
+          mbar_wait(sfree + 0, gj & 1);
+          tc_fence_after();
+          issue_qk_half(0, bn, 0);
+        }
         mbar_wait(vfull + b, SM::full_par(gj));
         mbar_wait(pfull + 0, gj & 1);
         tc_fence_after();
         KVQ_TRACE(gj, 8);
         issue_pv(0, b, j == 0);
-        if (j + 1 < np) {
-          mbar_wait(kfull + bn, SM::full_par(gj + 1));
-          tc_fence_after();
+        if (more) {
+          if (!kQkSplit) {
+            mbar_wait(kfull + bn, SM::full_par(gj + 1));
+            tc_fence_after();
+          }
           KVQ_TRACE(gj + 1, 9);
-          issue_qk(0, bn);
+          if (kQkSplit) issue_qk_half(0, bn, 1);
+          else issue_qk(0, bn);
           tc_commit(sfull + 0);
         } else {
           tc_commit(ofull + 0);
+        }
+        if (kQkSplit && more) {  // QK_1(j+1), keys 0-63
+          mbar_wait(sfree + 1, gj & 1);
+          tc_fence_after();
+          issue_qk_half(1, bn, 0);
         }
         mbar_wait(pfull + 1, gj & 1);
         tc_fence_after();
         KVQ_TRACE(gj, 10);
         issue_pv(1, b, j == 0);
         tc_commit(vempty + b);
-        if (j + 1 < np) {
-          issue_qk(1, bn);
+        if (more) {
+          if (kQkSplit) issue_qk_half(1, bn, 1);
+          else issue_qk(1, bn);
           KVQ_TRACE(gj + 1, 11);
           tc_commit(sfull + 1);
           tc_commit(kempty + bn);
@@ -1216,8 +1304,12 @@ __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ At
     if (p.out_dtype == DT_FP32) {
       *reinterpret_cast<float4*>((float*)p.O + ob) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     } else {
-      *reinterpret_cast<uint2*>((__nv_bfloat16*)p.O + ob) =
-          make_uint2(pack_bf162(acc.x * inv, acc.y * inv), pack_bf162(acc.z * inv, acc.w * inv));
+      __nv_bfloat16* dst = (__nv_bfloat16*)p.O + ob;
+      if (p.o_peer[0] != nullptr) {  // f4 direct: straight into the owning rank's O shard
+        const int r = t / p.o_Ts;
+        dst = reinterpret_cast<__nv_bfloat16*>(p.o_peer[r]) + ((int64_t)(t - r * p.o_Ts) * p.o_H + p.o_h0 + h) * D + 4 * c4;
+      }
+      *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf162(acc.x * inv, acc.y * inv), pack_bf162(acc.z * inv, acc.w * inv));
     }
   }
 }
@@ -1300,11 +1392,29 @@ cudaError_t launch_v2(AttnParams p, cudaStream_t st) {
 template <int D, bool SMOOTH>
 cudaError_t launch_nvfp4(const AttnParams& p, cudaStream_t st) {
   if (p.q_dtype == DT_FP32) return launch_t<D, true, false, SMOOTH, true>(p, st);
-  if (D == 128 && !SMOOTH && p.q_dtype == DT_BF16 && p.q_scale == nullptr && attn_v2_enabled()) return launch_v2(p, st);
+  if (D == 128 && !SMOOTH && p.q_dtype == DT_BF16 && p.q_scale == nullptr && p.o_peer[0] == nullptr && attn_v2_enabled())
+    return launch_v2(p, st);
   return launch_t<D, true, false, SMOOTH>(p, st);
 }
 
+template <int D>
+void touch_attention(cudaFuncAttributes* a) {
+  cudaFuncGetAttributes(a, attn_ws_kernel<D, true, false, false, false>);
+  cudaFuncGetAttributes(a, attn_ws_kernel<D, true, false, true, false>);
+  cudaFuncGetAttributes(a, attn_ws_kernel<D, true, false, false, true>);
+  cudaFuncGetAttributes(a, attn_ws_kernel<D, true, false, true, true>);
+  cudaFuncGetAttributes(a, combine_kernel<D>);
+}
+
 }  // namespace
+
+// module load of the NVFP4 attention kernels (see preload_quant_kernels)
+cudaError_t preload_attention_kernels() {
+  cudaFuncAttributes a;
+  touch_attention<128>(&a);
+  touch_attention<64>(&a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st) {
   if (nvfp4_kv && p.mean_k) return p.d == 128 ? launch_nvfp4<128, true>(p, st) : launch_nvfp4<64, true>(p, st);

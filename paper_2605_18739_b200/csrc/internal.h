@@ -67,6 +67,8 @@ struct ExportParams {
   float* mean_out;           // [T*H] t-major, or null
 };
 
+constexpr int kMaxP = 64;  // ranks of a Ulysses group
+
 struct AttnSeg {
   int32_t slot;   // cache slot (bf16kv mode: ignored)
   int32_t begin;  // first key row inside the slot
@@ -103,6 +105,10 @@ struct AttnParams {
   int units, qpairs, grid;
   bool hybrid;               // whole units in waves first, stream-K for the remainder (see Sched)
   int full_units;            // filled by launch_attention
+  // f4 direct: O row (t, h) is stored as bf16 into rank r = t / o_Ts's buffer o_peer[r] (a peer
+  // pointer, layout [o_Ts, o_H, d]) at row (t - r o_Ts, o_h0 + h); o_peer[0] null = O as usual
+  uint8_t* o_peer[kMaxP];
+  int o_Ts, o_H, o_h0;
   // bf16 KV mode: TMA tensor maps of K and V viewed as [n_keys][H][d] bf16, box {64, 1, 128},
   // 128-byte swizzle (one 128-key x 64-column panel of the K-major SW128 tile per copy)
   CUtensorMap tmap_k, tmap_v;
@@ -140,7 +146,6 @@ cudaError_t launch_ulysses_unpack_o(const uint8_t* recv, int dtype, int Ts, int 
 // from a source shard of Ts tokens for a destination owning Hp heads, rows (t, h_local) t-major:
 // [Q Ts*Hp*d*es][K codes Ts*Hp*d/2][K scales Ts*Hp*d/16][V codes][V scales][K means Ts*Hp*4 if
 // smoothing], every part padded to 16 bytes.
-constexpr int kMaxP = 64;
 struct Nvfp4SegLayout {
   int64_t q, qs, kc, ks, vc, vs, km, total;  // byte offsets within the segment, total size
 };
@@ -160,24 +165,36 @@ inline Nvfp4SegLayout nvfp4_seg_layout(int Ts, int Hp, int d, int es, bool smoot
   L.total = L.km + (smooth ? pad16(rows * 4) : 0);
   return L;
 }
+// Where the pack kernel stores destination r's rows (row = (token t of the shard, local head hl)):
+// Q rows (d * es bytes, or NVFP4 d/2 + d/16) at index t * q_ts + hl * q_hs, code rows (d/2 bytes),
+// scale rows (d/16) and K-smoothing means (fp32) at t * kv_ts + hl * kv_hs.  A staging segment is
+// t-major (kv_ts = q_ts = H_r, hs = 1); f4 direct stores into the owner's head-major cache slot
+// (kv_ts = 1, kv_hs = rows per head, bases at the slot's row rank * Ts).
+struct PackDest {
+  uint8_t *q, *qs, *kc, *ks, *vc, *vs;
+  float* km;
+  int64_t kv_ts, kv_hs, q_ts, q_hs;
+};
+inline PackDest pack_dest_segment(uint8_t* seg, const Nvfp4SegLayout& L, int Hp) {
+  return PackDest{seg + L.q, seg + L.qs, seg + L.kc, seg + L.ks, seg + L.vc, seg + L.vs,
+                  reinterpret_cast<float*>(seg + L.km), Hp, 1, Hp, 1};
+}
 struct PackNvfp4Params {
   const void* x[3];          // Q, K, V shards [Ts, H, d] (dtype)
   int dtype, Ts, H, d, P, mode;
   const float* amax;         // [2] global amax of K (K_bar with smoothing) and V over all ranks
   const float* amax_q;       // global amax of Q: Q travels as NVFP4 (plain R1 encoding); null: as is
-  uint8_t* send;
-  int64_t seg_off[kMaxP];    // byte offset of destination r's segment
-  Nvfp4SegLayout lay[kMaxP];  // its layout
+  PackDest dst[kMaxP];       // destination r's rows
   int h0[kMaxP + 1];
   uint8_t owner[256];
-  // f4 (peer memory): with dst[0] set, destination r's segment is stored straight into rank r's
-  // exchange window (dst[r], a peer pointer over NVLink); the global amax is the max of this
-  // rank's mailbox (P epoch-tagged entries, polled), and every CTA bumps each destination's arrival
-  // counter for this source (arrive[r], peer pointer) once its stores are done.
-  uint8_t* dst[kMaxP];
-  const unsigned long long* mailbox;  // [P][2] (epoch << 32 | amax bits)
+  // f4 (peer memory): with mailbox set, dst[] are peer pointers over NVLink; the global amax is the
+  // max of this rank's mailbox (P epoch-tagged entries, polled), and every CTA bumps each
+  // destination's arrival counter for this source (arrive[r], peer pointer) once its stores are done.
+  const unsigned long long* mailbox;  // [P][2] (epoch << 32 | amax bits), or null
   unsigned long long* arrive[kMaxP];
   unsigned long long epoch;
+  float* g_out;              // f4 direct: [2] g of this rank's own cache slot (from the mailbox), or null
+  DevStatus* status;         //   non-finite global amax -> KVQ_ENONFINITE there
 };
 struct ScatterNvfp4Params {
   const uint8_t* recv;       // P segments of equal size (this rank is every source's destination)
@@ -221,6 +238,19 @@ struct PeerPublishParams {
   unsigned long long epoch;
   int P;
 };
+// f4: one thread spins (acquire, system scope) until every one of n words at words[i * stride]
+// satisfies the mode: 0 = epoch tag (w >> 32) == target, 1 = w >= target, 2 = w == target.  A 1-CTA
+// kernel, so the heavy kernels that follow never spin (ranks simulated on one GPU cannot starve).
+struct PeerWaitParams {
+  const unsigned long long* words;
+  int n, stride, mode;
+  unsigned long long target;
+};
+cudaError_t launch_peer_wait(const PeerWaitParams& p, cudaStream_t st);
+// module loads of every kernel the f4 direct step launches (no lazy load while a wait is pending)
+cudaError_t preload_peer_kernels();
+cudaError_t preload_quant_kernels();
+cudaError_t preload_attention_kernels();
 cudaError_t launch_peer_publish(const PeerPublishParams& p, cudaStream_t st);
 cudaError_t launch_peer_signal(const PeerSignalParams& p, cudaStream_t st);
 cudaError_t launch_peer_pull_o(const PeerPullParams& p, cudaStream_t st);

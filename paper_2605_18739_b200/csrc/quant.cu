@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
   constexpr int es = DT == DT_BF16 ? 2 : 4;
   const int64_t nblk = (int64_t)p.Ts * p.H * kNB;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const bool peer = p.dst[0] != nullptr;
+  const bool peer = p.mailbox != nullptr;
   __shared__ float s_amax[2];
   if (peer) {  // f4: the global amax = max over this rank's mailbox, once all P entries are this epoch's
     if (threadIdx.x < 2) {
@@ -1044,8 +1044,15 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
       s_amax[threadIdx.x] = __uint_as_float(m);
     }
     __syncthreads();
+    if (p.g_out != nullptr && blockIdx.x == 0 && threadIdx.x < 2) {  // f4 direct: this rank's own slot g
+      const uint32_t ab = __float_as_uint(s_amax[threadIdx.x]) & 0x7FFFFFFFu;
+      if (ab >= 0x7F800000u) {
+        if (p.status) atomicCAS(&p.status->code, 0, -6 /* KVQ_ENONFINITE */);
+      } else {
+        p.g_out[threadIdx.x] = ab == 0 ? 1.0f : __fdiv_rn(__uint_as_float(ab), 2688.0f);
+      }
+    }
   }
-  auto seg_of = [&](int r) { return peer ? p.dst[r] : p.send + p.seg_off[r]; };
   // ---- Q rows: NVFP4 (plain R1, the global amax_q) or passed through (16-byte chunks)
   if (p.amax_q) {
     const uint32_t qbits = __float_as_uint(p.amax_q[0]) & 0x7FFFFFFFu;
@@ -1064,11 +1071,10 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
         const int j = (int)(u - row * kNB);
         const int tt = (int)(row / p.H), h = (int)(row - (int64_t)tt * p.H);
         const int r = p.owner[h];
-        const int Hp = p.h0[r + 1] - p.h0[r];
-        const int64_t orow = (int64_t)tt * Hp + (h - p.h0[r]);
-        uint8_t* seg = seg_of(r);
-        *reinterpret_cast<uint2*>(seg + p.lay[r].q + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
-        seg[p.lay[r].qs + orow * kNB + j] = (uint8_t)sb[0];
+        const PackDest& ds = p.dst[r];
+        const int64_t orow = (int64_t)tt * ds.q_ts + (int64_t)(h - p.h0[r]) * ds.q_hs;
+        *reinterpret_cast<uint2*>(ds.q + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
+        ds.qs[orow * kNB + j] = (uint8_t)sb[0];
       }
     }
   } else {
@@ -1079,9 +1085,9 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
       const int cc = (int)(i - row * cpr);
       const int t = (int)(row / p.H), h = (int)(row - (int64_t)t * p.H);
       const int r = p.owner[h];
-      const int Hp = p.h0[r + 1] - p.h0[r];
+      const PackDest& ds = p.dst[r];
       const uint4 v = __ldg(reinterpret_cast<const uint4*>((const uint8_t*)p.x[0] + row * D * es) + cc);
-      uint8_t* o = seg_of(r) + p.lay[r].q + ((int64_t)t * Hp + (h - p.h0[r])) * D * es;
+      uint8_t* o = ds.q + ((int64_t)t * ds.q_ts + (int64_t)(h - p.h0[r]) * ds.q_hs) * D * es;
       reinterpret_cast<uint4*>(o)[cc] = v;
     }
   }
@@ -1119,12 +1125,11 @@ __global__ void __launch_bounds__(256) pack_nvfp4_kernel(const __grid_constant__
       const int j = (int)(u - row * kNB);
       const int tt = (int)(row / p.H), h = (int)(row - (int64_t)tt * p.H);
       const int r = p.owner[h];
-      const int Hp = p.h0[r + 1] - p.h0[r];
-      const int64_t orow = (int64_t)tt * Hp + (h - p.h0[r]);
-      uint8_t* seg = seg_of(r);
-      *reinterpret_cast<uint2*>(seg + (t ? p.lay[r].vc : p.lay[r].kc) + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
-      seg[(t ? p.lay[r].vs : p.lay[r].ks) + orow * kNB + j] = (uint8_t)sb[0];
-      if (smooth_t && j == 0) reinterpret_cast<float*>(seg + p.lay[r].km)[orow] = mean;
+      const PackDest& ds = p.dst[r];
+      const int64_t orow = (int64_t)tt * ds.kv_ts + (int64_t)(h - p.h0[r]) * ds.kv_hs;
+      *reinterpret_cast<uint2*>((t ? ds.vc : ds.kc) + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
+      (t ? ds.vs : ds.ks)[orow * kNB + j] = (uint8_t)sb[0];
+      if (smooth_t && j == 0) ds.km[orow] = mean;
     }
   }
   if (peer) {  // this CTA's stores are done: make them visible system-wide, then count the arrival
@@ -1443,6 +1448,29 @@ cudaError_t launch_ulysses_pack_nvfp4(const PackNvfp4Params& p, cudaStream_t st)
   const int grid = ulysses_pack_grid(p.Ts, p.H, p.d);
   if (p.dtype == DT_BF16) return p.d == 128 ? pack_nvfp4_mode<DT_BF16, 128>(p, grid, st) : pack_nvfp4_mode<DT_BF16, 64>(p, grid, st);
   return p.d == 128 ? pack_nvfp4_mode<DT_FP32, 128>(p, grid, st) : pack_nvfp4_mode<DT_FP32, 64>(p, grid, st);
+}
+
+// Force the module load of every kernel the f4 exchange step launches (cudaFuncGetAttributes loads a
+// lazily-loaded kernel): under CUDA lazy loading, the first launch of a kernel may wait for the
+// device's in-flight work, which must never happen while a device-side wait is pending.
+template <int DT, int D>
+static void touch_pack(cudaFuncAttributes* a) {
+  cudaFuncGetAttributes(a, pack_nvfp4_kernel<DT, D, 0>);
+  cudaFuncGetAttributes(a, pack_nvfp4_kernel<DT, D, 1>);
+  cudaFuncGetAttributes(a, pack_nvfp4_kernel<DT, D, 2>);
+  cudaFuncGetAttributes(a, pack_nvfp4_kernel<DT, D, 3>);
+  cudaFuncGetAttributes(a, smooth_amax_kernel<DT, D>);
+}
+cudaError_t preload_quant_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, amax_kernel<DT_BF16>);
+  cudaFuncGetAttributes(&a, amax_kernel<DT_FP32>);
+  cudaFuncGetAttributes(&a, reduce_partials_kernel);
+  touch_pack<DT_BF16, 128>(&a);
+  touch_pack<DT_BF16, 64>(&a);
+  touch_pack<DT_FP32, 128>(&a);
+  touch_pack<DT_FP32, 64>(&a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_probe(int which, const void* in, void* out, int64_t n, cudaStream_t st) {

@@ -195,6 +195,20 @@ __global__ void __launch_bounds__(256) scatter_nvfp4_kernel(const __grid_constan
   }
 }
 
+// f4: one thread waits for n peer-written words (see PeerWaitParams)
+__global__ void peer_wait_kernel(const __grid_constant__ PeerWaitParams p) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < p.n; ++i) {
+    for (;;) {
+      unsigned long long a;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p.words + (int64_t)i * p.stride) : "memory");
+      const bool ok = p.mode == 0 ? (a >> 32) == p.target : (p.mode == 1 ? a >= p.target : a == p.target);
+      if (ok) break;
+      __nanosleep(64);
+    }
+  }
+}
+
 // f4: this rank's shard amax, epoch-tagged, into its entry pair of every peer's mailbox
 __global__ void peer_publish_kernel(const __grid_constant__ PeerPublishParams p) {
   const int r = threadIdx.x >> 1, t = threadIdx.x & 1;
@@ -258,6 +272,19 @@ void partition_impl(int H, int P, int* h0, uint8_t* owner) {
 }  // namespace
 
 void ulysses_partition(int H, int P, int* h0, uint8_t* owner) { partition_impl(H, P, h0, owner); }
+
+cudaError_t preload_peer_kernels() {  // see preload_quant_kernels
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, peer_wait_kernel);
+  cudaFuncGetAttributes(&a, peer_publish_kernel);
+  cudaFuncGetAttributes(&a, peer_signal_kernel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const PeerWaitParams& p, cudaStream_t st) {
+  peer_wait_kernel<<<1, 32, 0, st>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_publish(const PeerPublishParams& p, cudaStream_t st) {
   peer_publish_kernel<<<1, 2 * kMaxP, 0, st>>>(p);

@@ -115,6 +115,11 @@ _SIGS = {
     "kv_append_peer": (ctypes.c_int, [_P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _P, _P]),
     "kvq_peer_signal_o": (ctypes.c_int, [_P, ctypes.c_int64, _P]),
     "kvq_peer_pull_o": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P]),
+    "kvq_peer_bind_caches": (ctypes.c_int, [_P, _P, _P]),
+    "kv_append_peer_direct": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, ctypes.c_int64, _P]),
+    "chunk_attention_peer": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(_Mask), ctypes.c_float,
+                                            ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    "kvq_peer_wait_o": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.POINTER(_P), _P]),
     "kvq_cache_get_config": (ctypes.c_int, [_P, ctypes.POINTER(Config)]),
     "kvq_get_unique_id": (ctypes.c_int, [_P]),
     "kvq_comm_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)]),
@@ -179,9 +184,11 @@ class KVCache:
 
     def __init__(self, num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk,
                  sink_frames=0, window_frames=None, max_chunk_slots=8, device=None,
-                 scale_search=False, k_smoothing=False):
+                 scale_search=False, k_smoothing=False, arena=None):
         """scale_search: Four-Over-Six block scales for K and V (PAPER.md:146, 728-739);
-        k_smoothing: keys stored mean-centred per (t, h), means restored."""
+        k_smoothing: keys stored mean-centred per (t, h), means restored (PAPER.md:139-145);
+        arena: a caller-allocated uint8 device tensor of >= cache_bytes(...) (e.g. torch symmetric
+        memory for the f4 direct exchange), else one is allocated."""
         L = lib()
         window_frames = window_frames if window_frames is not None else max_chunk_slots * frames_per_chunk
         self.cfg = Config(num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk, sink_frames,
@@ -191,7 +198,14 @@ class KVCache:
         if nbytes == 0:
             raise KVQError(-1, "kvq_cache_bytes (bad config)")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.arena = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        if arena is not None:
+            if arena.dtype != torch.uint8 or arena.numel() < nbytes or arena.device != self.device:
+                raise KVQError(-1, "arena: uint8 tensor of >= cache bytes on the cache's device")
+            self.arena = arena
+        else:
+            self.arena = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.T_c = tokens_per_frame * frames_per_chunk
         self.H, self.d = num_heads, head_dim
         h = ctypes.c_void_p()
@@ -452,6 +466,16 @@ def ulysses_pack_nvfp4(Q, K, V, P, amax_kv, scale_search=False, k_smoothing=Fals
     return send, sizes
 
 
+def cache_bytes(num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk, sink_frames=0,
+                window_frames=None, max_chunk_slots=8, scale_search=False, k_smoothing=False):
+    """kvq_cache_bytes: device arena bytes of a KVCache with this geometry (e.g. to allocate it in
+    torch symmetric memory for the f4 direct exchange)."""
+    window_frames = window_frames if window_frames is not None else max_chunk_slots * frames_per_chunk
+    cfg = Config(num_layers, num_heads, head_dim, tokens_per_frame, frames_per_chunk, sink_frames, window_frames,
+                 max_chunk_slots, 1 if scale_search else 0, 1 if k_smoothing else 0)
+    return int(lib().kvq_cache_bytes(ctypes.byref(cfg)))
+
+
 def peer_window_bytes(T_c, H, d, P, q_dtype=torch.bfloat16, k_smoothing=False):
     return int(lib().kvq_peer_window_bytes(T_c, H, d, P, _out_code(q_dtype), int(k_smoothing)))
 
@@ -506,6 +530,30 @@ class PeerExchange:
     def pull_o(self, epoch, out):
         _check(lib().kvq_peer_pull_o(self._h, epoch, _ptr(out), _stream()), "kvq_peer_pull_o")
         return out
+
+    # ---- f4 direct (include/kvq.h): owners' cache slots and O shards written in place
+    def bind_caches(self, cache, arena_ptrs):
+        """cache: this rank's KVCache; arena_ptrs: the P ranks' cache arena addresses seen from here."""
+        arr = (_P * self.P)(*[ctypes.c_void_p(int(a)) for a in arena_ptrs])
+        _check(lib().kvq_peer_bind_caches(self._h, cache._h, arr), "kvq_peer_bind_caches")
+        self.cache = cache
+
+    def append_direct(self, layer, chunk_index, Q, K, V, epoch):
+        _check(lib().kv_append_peer_direct(self._h, layer, chunk_index, _ptr(Q), _ptr(K), _ptr(V), epoch, _stream()),
+               "kv_append_peer_direct")
+
+    def attention_direct(self, layer, mask, epoch, softmax_scale=0.0, workspace=None):
+        m = mask._c()
+        _check(lib().chunk_attention_peer(self._h, layer, ctypes.byref(m), softmax_scale, epoch,
+                                          _ptr(workspace) if workspace is not None else None,
+                                          workspace.numel() if workspace is not None else 0, _stream()),
+               "chunk_attention_peer")
+
+    def wait_o(self, epoch):
+        """Address of this rank's O shard [T_c/P, H, d] bf16 for `epoch` (inside its window)."""
+        ptr = _P()
+        _check(lib().kvq_peer_wait_o(self._h, epoch, ctypes.byref(ptr), _stream()), "kvq_peer_wait_o")
+        return ptr.value
 
 
 class Ulysses:
@@ -563,6 +611,13 @@ class Ulysses:
             hdl = symm_mem.rendezvous(self.win, grp)
             self.peer = PeerExchange(T_c, H, d, world, rank, list(hdl.buffer_ptrs), dtype, cache.scale_search,
                                      cache.k_smoothing, device=dev)
+            # f4 direct: every rank's cache arena must be peer-accessible (torch symmetric memory)
+            try:
+                ahdl = symm_mem.rendezvous(cache.arena, grp)
+            except Exception as e:
+                raise ValueError("the peer exchange stores into the owners' caches: create the KVCache with "
+                                 "arena=symm_mem.empty(cache_bytes(...))") from e
+            self.peer.bind_caches(cache, list(ahdl.buffer_ptrs))
             self.epoch = 0
             torch.cuda.synchronize(dev)
             dist.barrier(group=grp)
@@ -595,25 +650,22 @@ class Ulysses:
         L, st = lib(), _stream()
         dt = _dt(Q)
         self._mark("start")
-        if self.peer is not None:  # f4: publish amax -> pack into peers' windows -> append -> attention -> pull O
+        if self.peer is not None:  # f4 direct: amax mailbox -> owners' cache slots -> attention -> owners' O
             self.epoch += 1
             ep, pe = self.epoch, self.peer
             pe.publish_amax(K, V, ep)
             self._mark("amax_publish")
-            pe.pack(Q, K, V, ep)
-            self._mark("quantize_pack_to_peers")
-            pe.append(self.cache, layer, chunk_index, ep, self.Q)
-            self._mark("scatter_append")
-            off = pe.o_local(ep) - self.win.data_ptr()
-            n = self.T_c * self.Hr * self.d * 2
-            O_loc = self.win[off:off + n].view(torch.bfloat16).view(self.T_c, self.Hr, self.d)
-            self.cache.attention(layer, self.Q, mask, out=O_loc)
-            self._mark("attention")
-            pe.signal_o(ep)
+            pe.append_direct(layer, chunk_index, Q, K, V, ep)
+            self._mark("quantize_store_to_owners")
+            pe.attention_direct(layer, mask, ep)
+            self._mark("attention_o_to_owners")
+            off = pe.wait_o(ep) - self.win.data_ptr()
+            n = self.Ts * self.H * self.d * 2
+            O_sh = self.win[off:off + n].view(torch.bfloat16).view(self.Ts, self.H, self.d)
+            self._mark("o_wait")
             if out is None:
-                out = torch.empty((self.Ts, self.H, self.d), dtype=torch.bfloat16, device=Q.device)
-            pe.pull_o(ep, out)
-            self._mark("o_pull")
+                return O_sh  # valid until this rank's step after next (epoch + 2)
+            out.copy_(O_sh)
             return out
         if self.nvfp4_kv:
             c, qn = self.cache, self.nvfp4_q

@@ -203,6 +203,76 @@ def test_peer_exchange_simulated_matches_single_gpu(P, H, search, smooth):
         assert np.abs(err).max() <= 2e-3 + np.abs(ref_o).max() * 2 ** -8
 
 
+@pytest.mark.parametrize("P,H,search,smooth,order", [(2, 12, False, False, -1), (4, 12, False, False, 1),
+                                                     (8, 12, False, False, -1), (3, 7, False, False, -1),
+                                                     (4, 12, True, True, -1)])
+def test_peer_direct_concurrent_ranks_match_single_gpu(P, H, search, smooth, order):
+    # §8(f) f4 as specified: the pack kernel stores each owner's NVFP4 rows straight into the owner's
+    # cache slot and the attention epilogue / combine store O rows straight into the token owner's
+    # shard (no scatter, no pull).  The P simulated ranks each run on their OWN stream and are issued
+    # rank P-1 first (order = -1), so every device-side wait (mailbox, arrivals, O-ready flags)
+    # really blocks on kernels of other streams that are issued later; each rank's O shard, cache
+    # bytes, g and K means must equal the single-GPU path's, O within the oracle bar.
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    tpf, fc, d = 40, 3, 128
+    T = tpf * fc
+    Ts = T // P
+    sink, window = 3, 9
+    parts = [kvq.head_partition(H, P, r) for r in range(P)]
+    mk = dict(sink_frames=sink, window_frames=window, max_chunk_slots=8, device=DEV, scale_search=search,
+              k_smoothing=smooth)
+    caches = [kvq.KVCache(1, h1 - h0, d, tpf, fc, **mk) for h0, h1 in parts]
+    ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
+    orc = OracleKVCache(1, H, d, tpf, fc, scale_search=search, k_smoothing=smooth)
+    wb = kvq.peer_window_bytes(T, H, d, P, k_smoothing=smooth)
+    wins = [torch.zeros(wb, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    ptrs = [w.data_ptr() for w in wins]
+    pes = [kvq.PeerExchange(T, H, d, P, r, ptrs, scale_search=search, k_smoothing=smooth) for r in range(P)]
+    for r in range(P):
+        pes[r].bind_caches(caches[r], [c.arena.data_ptr() for c in caches])
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ranks = list(range(P))[::order]
+    # torch's own kernels load lazily too: run the O copy once before any device-side wait is pending
+    scratch = torch.zeros((T, H, d), dtype=torch.bfloat16, device=DEV)
+    scratch[:Ts].copy_(scratch[Ts:2 * Ts])
+    torch.cuda.synchronize()
+    for ch in range(5):
+        ep = ch + 1
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 0, ch, variant="outlier" if ch % 2 else "iid")
+        Q, K, V = q.torch(DEV), k.torch(DEV), v.torch(DEV)
+        mask = kvq.Mask(ch, sink, window)
+        ref.append(0, ch, K, V)
+        orc.append(0, ch, k.f64, v.f64)
+        shards = [tuple(x[r * Ts:(r + 1) * Ts].contiguous() for x in (Q, K, V)) for r in range(P)]
+        O_full = torch.empty((T, H, d), dtype=torch.bfloat16, device=DEV)
+        torch.cuda.synchronize()
+        for r in ranks:  # one rank's whole step per stream, issued back to back, no host sync
+            with torch.cuda.stream(streams[r]):
+                pes[r].publish_amax(shards[r][1], shards[r][2], ep)
+                pes[r].append_direct(0, ch, *shards[r], ep)
+                pes[r].attention_direct(0, mask, ep)
+                ptr = pes[r].wait_o(ep)
+                off = ptr - wins[r].data_ptr()
+                O_full[r * Ts:(r + 1) * Ts].copy_(wins[r][off:off + Ts * H * d * 2].view(torch.bfloat16).view(Ts, H, d))
+        torch.cuda.synchronize()
+        ex = ref.export(0, ch)
+        for p, (h0, h1) in enumerate(parts):
+            e = caches[p].export(0, ch)
+            for name in ("codes_k", "scales_k", "codes_v", "scales_v"):
+                full = ex[name].view(T, H, -1)[:, h0:h1].reshape(-1, ex[name].shape[1])
+                assert torch.equal(e[name], full), (p, name)
+            assert torch.equal(e["g_k"], ex["g_k"]) and torch.equal(e["g_v"], ex["g_v"])
+            if smooth:
+                km = ref.export_kmean(0, ch).view(T, H)[:, h0:h1].reshape(-1)
+                assert torch.equal(caches[p].export_kmean(0, ch), km)
+        O_ref_b = ref.attention(0, Q, mask, torch.bfloat16)
+        assert torch.allclose(O_full.float(), O_ref_b.float(), rtol=1e-2, atol=2e-3)
+        ref_o = orc.attend(0, ch, q.f64, sink, window)
+        err = (O_full.float().cpu().numpy() - ref_o)
+        assert np.abs(err).max() <= 2e-3 + np.abs(ref_o).max() * 2 ** -8
+
+
 @pytest.mark.parametrize("exchange", ["bf16", "nvfp4", "peer", "nvfp4q"])
 def test_ulysses_class_world1_nccl(exchange):
     # The Ulysses orchestration bench.py runs at N > 1 (NCCL all-to-all / all-reduce, torch symmetric
@@ -225,7 +295,11 @@ def test_ulysses_class_world1_nccl(exchange):
         T = tpf * fc
         mk = dict(sink_frames=3, window_frames=9, max_chunk_slots=8, device=DEV)
         c_ref = kvq.KVCache(1, H, d, tpf, fc, **mk)
-        c_uly = kvq.KVCache(1, H, d, tpf, fc, **mk)
+        arena = None
+        if exchange == "peer":  # f4 direct writes the owners' caches: the arena lives in symmetric memory
+            import torch.distributed._symmetric_memory as symm_mem
+            arena = symm_mem.empty(kvq.cache_bytes(1, H, d, tpf, fc, 3, 9, 8), dtype=torch.uint8, device=DEV)
+        c_uly = kvq.KVCache(1, H, d, tpf, fc, arena=arena, **mk)
         uly = kvq.Ulysses(c_uly, H, d, T, 0, 1, nvfp4_kv=exchange == "nvfp4", peer=exchange == "peer",
                           nvfp4_q=exchange == "nvfp4q")
         for ch in range(4):

@@ -3,10 +3,11 @@
 # usage: bash tools/ab_attn.sh <rounds> "<src.cu> [nvcc flags]" ...   ("." = the tree's attention.cu)
 # TOOL=tools/trace_attn.py prints the CTA-0 timeline of each variant instead of the timings.
 ROUNDS=$1; shift
+VARIANTS=("$@")
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for r in $(seq 1 $ROUNDS); do
-  for v in "$@"; do
-    set -- $v; src=$1; shift; flags="$*"
+  for v in "${VARIANTS[@]}"; do
+    read -r src flags <<< "$v"
     [[ $src == . ]] && src=paper_2605_18739_b200/csrc/attention.cu
     nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -Iinclude \
        -Ipaper_2605_18739_b200/csrc $flags -c $src -o paper_2605_18739_b200/_build/attention.cu.o > /tmp/ab_build.log 2>&1 \
