@@ -57,13 +57,32 @@ constexpr int kPolyPairs = KVQ_POLY_PAIRS;
 #define KVQ_LAZY_LOG2 4.0f
 #endif
 constexpr float kLazyLog2 = KVQ_LAZY_LOG2;
-// Split QK (build knob): S_i = [keys 0-63 | keys 64-127] as two N = 64 MMAs, P_i (fp16) stored in
-// the upper 64 columns; QK_i(j+1)'s first half is issued as soon as softmax_i(j) has loaded S_i(j)
-// into registers (the `sfree` barrier), so only its second half waits for PV_i(j) to consume P_i(j).
-#ifndef KVQ_QK_SPLIT
-#define KVQ_QK_SPLIT 0
+// Rotating S/P regions (build knob, default on).  The 256 S/P columns of TMEM are four 64-column
+// regions R0..R3; the k-th QK of a piece (k = 2 j + tile) writes keys 0-63 into region a(k) and keys
+// 64-127 into region b(k) (two N = 64 MMAs), and the softmax stores P (fp16, 64 columns) into b(k).
+// a is free again as soon as the softmax has loaded S into registers (`sfree`), b once the PV that
+// reads P has been issued (the tensor core runs in issue order).  k = 0, 1: (R0, R1), (R2, R3); then
+// a = R0 and b cycles R2, R1, R3 -- each b is exactly the P region of the PV issued just before, so
+// QK_i(j+1) waits only for the OTHER tile's softmax to have loaded its S, not for PV_i(j): the next
+// scores are computed while this tile's softmax still runs, and each softmax warpgroup goes from one
+// tile to the next without waiting for its own PV + QK round trip.  Correct (parity suite) but
+// measured SLOWER (942 vs 914 us): the N = 64 halves re-read the whole Q tile per MMA, so a QK moves
+// 1.5x the shared-memory bytes of an N = 128 one (6 KB per 32-cycle MMA > 128 B/clk), and no
+// rotation keeps both halves of every S in adjacent regions.  Off by default.
+#ifndef KVQ_SP_ROTATE
+#define KVQ_SP_ROTATE 0
 #endif
-constexpr bool kQkSplit = KVQ_QK_SPLIT != 0;
+constexpr bool kRotate = KVQ_SP_ROTATE != 0;
+KVQ_DEV void sp_regions(int k, uint32_t& a, uint32_t& b) {
+  if (k < 2) {
+    a = 2u * k;
+    b = 2u * k + 1u;
+  } else {
+    const int m = (k - 2) % 3;
+    a = 0u;
+    b = m == 0 ? 2u : (m == 1 ? 1u : 3u);
+  }
+}
 // Store P of keys 0-63 to TMEM from inside the exponential loop (build knob), overlapping the
 // tcgen05.st with the second half of the loop (the MMA still waits for the whole tile's P).
 #ifndef KVQ_EARLY_STTM
@@ -102,7 +121,7 @@ struct WsSmem {
   static constexpr int kQL1 = D == 128 ? 5 * kTile : 7 * kTile;
   static constexpr int kBar = (QSPLIT && D != 128) ? 8 * kTile : 6 * kTile;
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
-  static constexpr int kMean = kBar + 18 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
+  static constexpr int kMean = kBar + 20 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
   static constexpr int kBytes = kMean + 2 * 2 * 128 * 4 + 1024;
   // K^/V^ buffer of global tile g, and the mbarrier parities of its full / empty waits
   static KVQ_DEV int buf(int g) { return kNBuf == 2 ? (g & 1) : 0; }
@@ -416,8 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
   uint64_t* pfull = bars + 10;  // [2] softmax WG i -> MMA (P_i written, O_i rescaled)
   uint64_t* ofull = bars + 12;  // [2] MMA -> softmax WG i (last PV_i of a piece done)
   uint64_t* qfull = bars + 14;  // [2] softmax WG i -> MMA (Q_i tile of a piece loaded)
-  uint64_t* sfree = bars + 16;  // [2] softmax WG i -> MMA (S_i loaded to registers; kQkSplit only)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* sfree = bars + 16;  // [2] softmax WG i -> MMA (S_i loaded to registers; kRotate only)
+  uint64_t* ofree = bars + 18;  // [2] MMA -> softmax WG i (PV_i of a tile done: O_i may be rescaled; kRotate)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int H = p.H;
@@ -437,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_init(ofull + b, 1);
       mbar_init(qfull + b, 128);
       mbar_init(sfree + b, 128);
+      mbar_init(ofree + b, 1);
     }
     fence_mbar_init();
   }
@@ -487,17 +508,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         KVQ_TRACE(g, 3 * qi + 1);
         tc_fence_after();
         uint32_t s[128];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) KVQ_TMEM_LD32(tS + 32 * cc, (s + 32 * cc));
+        uint32_t tSa = tS, tSb = tS + 64;  // S keys 0-63 / 64-127; P goes to tSb (kRotate) or tS
+        if (kRotate) {
+          uint32_t ra, rb;
+          sp_regions(2 * j + qi, ra, rb);
+          tSa = tmem + 64u * ra + lane_off;
+          tSb = tmem + 64u * rb + lane_off;
+        }
+        KVQ_TMEM_LD32(tSa, s);
+        KVQ_TMEM_LD32(tSa + 32, (s + 32));
+        KVQ_TMEM_LD32(tSb, (s + 64));
+        KVQ_TMEM_LD32(tSb + 32, (s + 96));
         if (SMOOTH) {  // share the tile's key means within the warpgroup (double-buffered)
           float* mbuf = reinterpret_cast<float*>(smem + SM::kMean) + (qi * 2 + (j & 1)) * 128;
           mbuf[row] = mean_r;
           asm volatile("bar.sync %0, 128;" ::"r"(1 + qi) : "memory");
         }
         tmem_ld_wait();
-        if (kQkSplit) {
+        if (kRotate) {
           tc_fence_before();
-          mbar_arrive(sfree + qi);  // S_i(j) is in registers: QK_i(j+1)'s first half may overwrite it
+          mbar_arrive(sfree + qi);  // S_i(j) is in registers: its region a may take the next QK
         }
         KVQ_TRACE_SM(g, 12);
         if (SMOOTH) {  // y = s * cs + m_j * sum(q) * scale_log2  (log2 units), in place
@@ -577,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
           }
           const uint32_t pk = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
           s[kk] = pk;
-          if (kEarlySttm && kk == 31) KVQ_TMEM_ST32(tS + (kQkSplit ? 64 : 0), s);  // keys 0-63 final: store now
+          if (kEarlySttm && kk == 31) KVQ_TMEM_ST32(kRotate ? tSb : tS, s);  // keys 0-63 final: store now
 #if defined(KVQ_SUM_UNROUNDED)
           if (kk & 1) acc1 = fadd2(acc1, f32x2_pack(p0, p1));
           else acc0 = fadd2(acc0, f32x2_pack(p0, p1));
@@ -598,10 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         f32x2_unpack(acc1, b0, b1);
         l_run = l_run * alpha + ((a0 + a1) + (b0 + b1)) + ((la[0] + la[1]) + (la[2] + la[3]));
         KVQ_TRACE_SM(g, 14);
-        if (!kEarlySttm) KVQ_TMEM_ST32(tS + (kQkSplit ? 64 : 0), s);
-        KVQ_TMEM_ST32(tS + (kQkSplit ? 96 : 32), (s + 32));
+        if (!kEarlySttm) KVQ_TMEM_ST32(kRotate ? tSb : tS, s);
+        KVQ_TMEM_ST32((kRotate ? tSb : tS) + 32, (s + 32));
         // O_i is kept in units of the current chunk's g_V: rescale by alpha * g_V,prev / g_V,new.
-        // PV_i(j-1) is complete here (issued before QK_i(j), whose commit we waited on).
+        // Without kRotate PV_i(j-1) is complete here (issued before QK_i(j), whose commit we waited on);
+        // with it, the rescale waits for PV_i(j-1)'s own commit (`ofree`).
 #ifdef KVQ_EXPERIMENT_NO_RESCALE
         if (false) {
 #else
@@ -609,6 +640,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #endif
           const float f = alpha * (gv_run / gv);
           if (!__all_sync(0xffffffffu, f == 1.0f)) {
+            if (kRotate) {  // this tile's QK no longer orders PV_i(j-1) before us: wait for it
+              mbar_wait(ofree + qi, (g - 1) & 1);
+              tc_fence_after();
+            }
             // two 32-column chunks per TMEM round trip, staged in the free half of s[]
             const uint64_t f2 = f32x2_pack(f, f);
 #pragma unroll
@@ -782,10 +817,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       }
       __syncwarp();
     };
-    // kQkSplit: keys [64 half, 64 half + 64) of the tile into S_i columns [64 half, +64)
-    auto issue_qk_half = [&](int qi, int b, int half) {
+    // kRotate: keys [64 half, 64 half + 64) of the K tile into the 64-column TMEM region `reg`
+    auto issue_qk_half = [&](int qi, int b, int half, uint32_t reg) {
       const uint64_t da = qi ? dQ1 : dQ0, db = (b ? dK1 : dK0) + (uint64_t)((8192 * half) >> 4);
-      const uint32_t dt = tmem + 128u * qi + 64u * half;
+      const uint32_t dt = tmem + 64u * reg;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -803,9 +838,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int qi, int b, bool first) {
+    // P_i at TMEM column pcol (kRotate: its region b; else S_i's first 64 columns)
+    auto issue_pv = [&](int qi, int b, bool first, uint32_t pcol) {
       const uint64_t db = b ? dV1 : dV0;
-      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + 128u * qi + (kQkSplit ? 64u : 0u);
+      const uint32_t dt = tmem + 256u + 128u * qi, ta = tmem + pcol;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -817,6 +853,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       if (elect_one()) kvq::tc_commit(bar);
       __syncwarp();
     };
+    auto qk_rot = [&](int qi, int b, int kq) {  // the kq-th QK of the piece (tile qi) into its regions
+      uint32_t ra, rb;
+      sp_regions(kq, ra, rb);
+      issue_qk_half(qi, b, 0, ra);
+      issue_qk_half(qi, b, 1, rb);
+    };
+    auto p_col = [&](int kq) -> uint32_t {
+      uint32_t ra, rb;
+      sp_regions(kq, ra, rb);
+      return 64u * rb;
+    };
     int g = 0;
     Piece pc;
     for (int k = 0; get_piece(sch, c, k, pc); ++k) {
@@ -825,50 +872,88 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_wait(qfull + 1, k & 1);
       mbar_wait(kfull + SM::buf(g), SM::full_par(g));
       tc_fence_after();
-      issue_qk(0, SM::buf(g));
+      if (kRotate) qk_rot(0, SM::buf(g), 0);
+      else issue_qk(0, SM::buf(g));
       tc_commit(sfull + 0);
-      issue_qk(1, SM::buf(g));
+      if (kRotate) qk_rot(1, SM::buf(g), 1);
+      else issue_qk(1, SM::buf(g));
       tc_commit(sfull + 1);
       tc_commit(kempty + SM::buf(g));
       for (int j = 0; j < np; ++j) {
         const int gj = g + j, b = SM::buf(gj), bn = SM::buf(gj + 1);
         const bool more = j + 1 < np;
-        if (kQkSplit && more) {  // QK_0(j+1), keys 0-63, while softmax_0(j) runs
-          mbar_wait(kfull + bn, SM::full_par(gj + 1));
-          mbar_wait(sfree + 0, gj & 1);
-          tc_fence_after();
-          issue_qk_half(0, bn, 0);
+        if (kRotate) {
+          // Four issues per tile pair, each as soon as its inputs are ready (polled: the whole warp reads
+          // lane 0's non-blocking barrier tests), in two rounds so that every QK follows the PV whose P
+          // region it reuses:
+          //   [A] QK_0(j+1): region a = R0 held S_1(j) (j >= 1; j = 0: S_0(0), and S_1(0)'s R2 is its b) ->
+          //       needs softmax_1 to have loaded S_1(j); region b = P_1(j-1)'s (PV_1(j-1) issued last round)
+          //   [B] PV_0(j): needs P_0(j) and V(j)
+          //   [C] QK_1(j+1): a = R0 held S_0(j+1) -> needs softmax_0 to have loaded it; b = P_0(j)'s ([B])
+          //   [D] PV_1(j): needs P_1(j)
+          auto ready = [&](bool c) { return __shfl_sync(0xffffffffu, c ? 1 : 0, 0) != 0; };
+          bool doneA = !more, doneB = false;
+          while (!(doneA && doneB)) {
+            if (!doneA && ready(mbar_test(kfull + bn, SM::full_par(gj + 1)) &&
+                                (j != 0 || mbar_test(sfree + 0, gj & 1)) && mbar_test(sfree + 1, gj & 1))) {
+              tc_fence_after();
+              KVQ_TRACE(gj + 1, 9);
+              qk_rot(0, bn, 2 * j + 2);
+              tc_commit(sfull + 0);
+              doneA = true;
+            }
+            if (!doneB && ready(mbar_test(vfull + b, SM::full_par(gj)) && mbar_test(pfull + 0, gj & 1))) {
+              tc_fence_after();
+              KVQ_TRACE(gj, 8);
+              issue_pv(0, b, j == 0, p_col(2 * j));
+              tc_commit(ofree + 0);
+              if (!more) tc_commit(ofull + 0);
+              doneB = true;
+            }
+          }
+          bool doneC = !more, doneD = false;
+          while (!(doneC && doneD)) {
+            if (!doneC && ready(mbar_test(sfree + 0, (gj + 1) & 1))) {
+              tc_fence_after();
+              qk_rot(1, bn, 2 * j + 3);
+              KVQ_TRACE(gj + 1, 11);
+              tc_commit(sfull + 1);
+              tc_commit(kempty + bn);
+              doneC = true;
+            }
+            if (!doneD && ready(mbar_test(pfull + 1, gj & 1))) {
+              tc_fence_after();
+              KVQ_TRACE(gj, 10);
+              issue_pv(1, b, j == 0, p_col(2 * j + 1));
+              tc_commit(vempty + b);
+              tc_commit(ofree + 1);
+              if (!more) tc_commit(ofull + 1);
+              doneD = true;
+            }
+          }
+          continue;
         }
         mbar_wait(vfull + b, SM::full_par(gj));
         mbar_wait(pfull + 0, gj & 1);
         tc_fence_after();
         KVQ_TRACE(gj, 8);
-        issue_pv(0, b, j == 0);
+        issue_pv(0, b, j == 0, 0u);
         if (more) {
-          if (!kQkSplit) {
-            mbar_wait(kfull + bn, SM::full_par(gj + 1));
-            tc_fence_after();
-          }
+          mbar_wait(kfull + bn, SM::full_par(gj + 1));
+          tc_fence_after();
           KVQ_TRACE(gj + 1, 9);
-          if (kQkSplit) issue_qk_half(0, bn, 1);
-          else issue_qk(0, bn);
+          issue_qk(0, bn);
           tc_commit(sfull + 0);
         } else {
           tc_commit(ofull + 0);
         }
-        if (kQkSplit && more) {  // QK_1(j+1), keys 0-63
-          mbar_wait(sfree + 1, gj & 1);
-          tc_fence_after();
-          issue_qk_half(1, bn, 0);
-        }
         mbar_wait(pfull + 1, gj & 1);
         tc_fence_after();
         KVQ_TRACE(gj, 10);
-        issue_pv(1, b, j == 0);
+        issue_pv(1, b, j == 0, 128u);
         tc_commit(vempty + b);
         if (more) {
-          if (kQkSplit) issue_qk_half(1, bn, 1);
-          else issue_qk(1, bn);
+          issue_qk(1, bn);
           KVQ_TRACE(gj + 1, 11);
           tc_commit(sfull + 1);
           tc_commit(kempty + bn);
