@@ -157,6 +157,24 @@ kvq_status chunk_attention_ws(kvq_cache* cache, int32_t layer, const void* Q, kv
                               kvq_dtype out_dtype, void* dev_workspace, size_t workspace_bytes,
                               void* stream);
 
+/* kv_quantize_append of chunk `chunk_index` followed by chunk_attention of its queries, as ONE
+ * launch: the three spare warps of every attention CTA quantize that CTA's share of K and V into
+ * the chunk's slot (the same bytes as kv_quantize_append, reading Z4 definition R1) while the other
+ * warps attend over the history; each CTA reads the new slot only after every CTA has finished
+ * (the tensor amax is exchanged between the co-resident CTAs of a cooperative launch), and a
+ * first work piece that would reach the new chunk's tiles early is processed last.  The append's
+ * own time is hidden behind the history tiles (PAPER.md:146's "<2%" overhead, made ~0).
+ * mask->chunk_index must equal chunk_index.  Used when the cache is in the plain mode
+ * (scale_mode 0, no K-smoothing), Q is bf16 and the appended chunk is at most half of K_eff;
+ * otherwise the call runs kv_quantize_append then chunk_attention(_ws) on the stream.  Errors as
+ * for those two calls (checked before anything is launched).  dev_workspace: NULL = the cache's
+ * own, else as chunk_attention_ws. */
+kvq_status chunk_attention_append(kvq_cache* cache, int32_t layer, int64_t chunk_index,
+                                  const void* K, const void* V, kvq_dtype in_dtype, const void* Q,
+                                  kvq_dtype q_dtype, const kvq_mask* mask, float softmax_scale,
+                                  void* O, kvq_dtype out_dtype, void* dev_workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* Checking: dequantize one resident chunk to dev [T_c, H, d]: FP32 = RN32(dec(c) dec(s) g)
  * (Eq. 2), BF16 = RN_bf16 of that.  With k_smoothing, K = RN32(dec(c) dec(s) g + mean)
  * (one rounding). */

@@ -37,7 +37,7 @@ def _nccl():
     except ImportError:
         pass
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
-HEADERS = ["common.cuh", "internal.h"]
+HEADERS = ["common.cuh", "internal.h", "quant_core.cuh"]
 
 
 def _mtime(p):

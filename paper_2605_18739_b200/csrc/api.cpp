@@ -27,7 +27,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t T_c, T_pad, rows_per_head;  // rows_per_head = slots * T_pad
   size_t codes_bytes, scales_bytes;   // per tensor (K or V), all layers
-  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_counters, off_ws, total;
+  size_t off_codes[2], off_scales[2], off_g, off_partials, off_status, off_counters, off_ws, off_apsync, total;
   size_t off_mean, mean_bytes;        // K-smoothing row means [L][H][rows_per_head] fp32 (0 if off)
 };
 
@@ -63,6 +63,7 @@ Layout make_layout(const kvq_config* c) {
   L.off_counters = off;  // grid-barrier slots of the single-pass quantizer: [CTA][K|V] u64
   off += align_up((size_t)kMaxFusedCtas * kSlotU64 * sizeof(unsigned long long), kAlign);
   L.off_ws = off; off += align_up(attn_ws_bytes(c->head_dim), kAlign);
+  L.off_apsync = off; off += align_up(kApSyncWords * sizeof(unsigned long long), kAlign);  // fused append
   L.mean_bytes = c->k_smoothing ? align_up((size_t)rows * sizeof(float), kAlign) : 0;
   L.off_mean = off; off += L.mean_bytes;
   L.total = off;
@@ -397,9 +398,15 @@ struct AttnRoute {  // f4 direct: O rows into the owning ranks' O shards (AttnPa
   uint8_t* const* o_peer;
   int P, Ts, H, h0;
 };
+struct AttnAppend {  // chunk_attention_append: the chunk's K, V quantized inside the attention launch
+  const void* K;
+  const void* V;
+  int dtype, slot;
+};
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
                                  const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
-                                 size_t ws_bytes, void* stream, const AttnRoute* route = nullptr);
+                                 size_t ws_bytes, void* stream, const AttnRoute* route = nullptr,
+                                 const AttnAppend* app = nullptr);
 
 kvq_status chunk_attention(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
                            float softmax_scale, void* O, kvq_dtype out_dtype, void* stream) {
@@ -419,6 +426,44 @@ kvq_status chunk_attention_ws(kvq_cache* c, int32_t layer, const void* Q, kvq_dt
                         workspace_bytes, stream);
 }
 
+kvq_status chunk_attention_append(kvq_cache* c, int32_t layer, int64_t chunk_index, const void* K, const void* V,
+                                  kvq_dtype in_dtype, const void* Q, kvq_dtype q_dtype, const kvq_mask* mask,
+                                  float softmax_scale, void* O, kvq_dtype out_dtype, void* dev_workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (!c || !K || !V || !Q || !O || !mask) return KVQ_EINVAL;
+  if (in_dtype != KVQ_BF16 && in_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (q_dtype != KVQ_BF16 && q_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (out_dtype != KVQ_BF16 && out_dtype != KVQ_FP32) return KVQ_EDTYPE;
+  if (mask->chunk_index != chunk_index) return KVQ_EINVAL;  // the call attends the chunk it appends
+  if (dev_workspace && ((reinterpret_cast<uintptr_t>(dev_workspace) % kAlign) != 0 ||
+                        workspace_bytes < kvq_attention_workspace_bytes(c)))
+    return KVQ_EINVAL;
+  const kvq_status v = validate_append_attend(c, layer, chunk_index, mask);  // host dry run: nothing launched on error
+  if (v != KVQ_OK) return v;
+  // fused only where it pays: plain NVFP4 (no 4/6 search, no K-smoothing), bf16 queries, and a key set
+  // of which the appended chunk is at most half (the history tiles hide the append); else the two calls
+  int64_t n_keys = 0;
+  for (auto& iv : key_token_ranges(mask->chunk_index, c->cfg.frames_per_chunk, c->cfg.tokens_per_frame,
+                                   mask->sink_frames, mask->window_frames, mask->shot_start_frame, mask->shot_len_frames))
+    n_keys += iv.second - iv.first;
+  const bool fuse = c->cfg.scale_mode == 0 && !c->cfg.k_smoothing && q_dtype == KVQ_BF16 && !c->two_pass_only &&
+                    2 * c->L.T_c <= n_keys;
+  if (!fuse) {
+    const kvq_status s = kv_quantize_append(c, layer, chunk_index, K, V, in_dtype, stream);
+    if (s != KVQ_OK) return s;
+    return dev_workspace ? chunk_attention_ws(c, layer, Q, q_dtype, mask, softmax_scale, O, out_dtype, dev_workspace,
+                                              workspace_bytes, stream)
+                         : chunk_attention(c, layer, Q, q_dtype, mask, softmax_scale, O, out_dtype, stream);
+  }
+  SlotPlan plan;
+  const kvq_status ss = select_slot(c, layer, chunk_index, &plan);
+  if (ss != KVQ_OK) return ss;
+  commit_slot(c, layer, chunk_index, plan);  // the key set below includes the chunk being appended
+  const AttnAppend app{K, V, in_dtype == KVQ_BF16 ? DT_BF16 : DT_FP32, plan.slot};
+  return attention_impl(c, layer, Q, q_dtype, nullptr, mask, softmax_scale, O, out_dtype, dev_workspace,
+                        workspace_bytes, stream, nullptr, &app);
+}
+
 kvq_status chunk_attention_qscaled(kvq_cache* c, int32_t layer, const void* Q_fp16, const float* dev_q_scale,
                                    const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype,
                                    void* stream) {
@@ -429,7 +474,7 @@ kvq_status chunk_attention_qscaled(kvq_cache* c, int32_t layer, const void* Q_fp
 
 static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq_dtype q_dtype, const float* q_scale,
                                  const kvq_mask* mask, float softmax_scale, void* O, kvq_dtype out_dtype, void* ws,
-                                 size_t ws_bytes, void* stream, const AttnRoute* route) {
+                                 size_t ws_bytes, void* stream, const AttnRoute* route, const AttnAppend* app) {
   (void)ws_bytes;
   if (!c || !Q || !O || !mask) return KVQ_EINVAL;
   if (layer < 0 || layer >= c->cfg.num_layers || mask->chunk_index < 0) return KVQ_EINVAL;
@@ -471,6 +516,19 @@ static kvq_status attention_impl(kvq_cache* c, int32_t layer, const void* Q, kvq
     p.o_Ts = route->Ts;
     p.o_H = route->H;
     p.o_h0 = route->h0;
+  }
+  if (app) {
+    p.ap_x[0] = app->K;
+    p.ap_x[1] = app->V;
+    p.ap_dtype = app->dtype;
+    p.ap_slot = app->slot;
+    for (int t = 0; t < 2; ++t) {
+      p.ap_codes[t] = codes_base(c, t, layer) + (size_t)app->slot * c->L.T_pad * (d / 2);
+      p.ap_scales[t] = scales_base(c, t, layer) + (size_t)app->slot * c->L.T_pad * (d / 16);
+    }
+    p.ap_g = g_base(c, layer) + app->slot * 2;
+    p.ap_sync = reinterpret_cast<unsigned long long*>(c->arena + c->L.off_apsync);
+    return cuda_status(launch_attention_append(p, S(stream)));
   }
   return cuda_status(launch_attention(p, true, S(stream)));
 }

@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "quant_core.cuh"
 
 namespace kvq {
 namespace {
@@ -46,6 +47,15 @@ constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant,
 #define KVQ_REG_MMA (256 - KVQ_REG_SOFTMAX)
 #endif
 constexpr int kRegSoftmax = KVQ_REG_SOFTMAX, kRegMma = KVQ_REG_MMA, kRegDequant = 512 - 2 * KVQ_REG_SOFTMAX - KVQ_REG_MMA;
+// the fused-append kernel (APPEND) carries a little more state through the softmax loop
+#ifndef KVQ_REG_SOFTMAX_AP
+#define KVQ_REG_SOFTMAX_AP 184
+#endif
+#ifndef KVQ_REG_MMA_AP
+#define KVQ_REG_MMA_AP 72
+#endif
+constexpr int kRegSoftmaxAp = KVQ_REG_SOFTMAX_AP, kRegMmaAp = KVQ_REG_MMA_AP,
+              kRegDequantAp = 512 - 2 * KVQ_REG_SOFTMAX_AP - KVQ_REG_MMA_AP;
 // Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
 // FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
 #ifndef KVQ_POLY_PAIRS
@@ -122,7 +132,8 @@ struct WsSmem {
   static constexpr int kBar = (QSPLIT && D != 128) ? 8 * kTile : 6 * kTile;
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
   static constexpr int kMean = kBar + 20 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
-  static constexpr int kBytes = kMean + 2 * 2 * 128 * 4 + 1024;
+  static constexpr int kAp = kMean + 2 * 2 * 128 * 4;  // fused append: launch epoch, shard amax partials
+  static constexpr int kBytes = kAp + 64 + 1024;
   // K^/V^ buffer of global tile g, and the mbarrier parities of its full / empty waits
   static KVQ_DEV int buf(int g) { return kNBuf == 2 ? (g & 1) : 0; }
   static KVQ_DEV uint32_t full_par(int g) { return kNBuf == 2 ? ((g >> 1) & 1) : (g & 1); }
@@ -150,16 +161,19 @@ struct PackedRow {
   uint32_t s[D / 64 > 0 ? D / 64 : 1];
 };
 
-template <int D>
+// CG: L2 loads (__ldcg) for rows written during this launch (the fused append's slot), else the
+// read-only path.
+template <int D, bool CG = false>
 KVQ_DEV void load_packed_row(PackedRow<D>& r, const uint8_t* crow, const uint8_t* srow) {
 #pragma unroll
-  for (int k = 0; k < D / 32; ++k) r.c[k] = __ldg(reinterpret_cast<const uint4*>(crow) + k);
+  for (int k = 0; k < D / 32; ++k)
+    r.c[k] = CG ? __ldcg(reinterpret_cast<const uint4*>(crow) + k) : __ldg(reinterpret_cast<const uint4*>(crow) + k);
   if (D == 128) {
-    uint2 s2 = __ldg(reinterpret_cast<const uint2*>(srow));
+    uint2 s2 = CG ? __ldcg(reinterpret_cast<const uint2*>(srow)) : __ldg(reinterpret_cast<const uint2*>(srow));
     r.s[0] = s2.x;
     r.s[1] = s2.y;
   } else {
-    r.s[0] = __ldg(reinterpret_cast<const uint32_t*>(srow));
+    r.s[0] = CG ? __ldcg(reinterpret_cast<const uint32_t*>(srow)) : __ldg(reinterpret_cast<const uint32_t*>(srow));
   }
 }
 
@@ -410,11 +424,157 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
       p.trace[(tile) * 16 + (ev)] = clock64();                                                   \
   } while (0)
 
+// ---------------------------------------------------------------------------------------------
+// Append fused into the attention launch (AttnParams::ap_*; kv_quantize_append's bytes exactly:
+// definition R1 through quant_core.cuh, whose arithmetic is explicit round-to-nearest intrinsics).
+KVQ_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+KVQ_DEV void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+KVQ_DEV float ld_relaxed_f32(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+KVQ_DEV unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// The nthreads threads of a group (lane `lt`) together wait until every CTA's done tag of this launch
+// (epoch E) is set: each polls its own tags with relaxed loads (an acquire per poll costs ~0.3 us;
+// 148 of them in sequence were 40 us), then one acquire fence; the caller then syncs the group.
+KVQ_DEV void ap_wait_all_done(const unsigned long long* sync, int G, unsigned long long E, int lt, int nthreads) {
+  for (int i = lt; i < G; i += nthreads)
+    while (ld_relaxed_u64(sync + 1 + 2 * kMaxCtas + i) != E + 1) __nanosleep(64);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// flat index of the first non-finite element of a block (rare path)
+template <int DT>
+KVQ_DEV int first_nonfinite16(const uint8_t* src) {
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t b = DT == DT_BF16 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[e] & 0x7FFFu) << 16
+                                     : reinterpret_cast<const uint32_t*>(src)[e] & 0x7FFFFFFFu;
+    if (b >= 0x7F800000u) return e;
+  }
+  return 0;
+}
+
+// Warps 13-15 of CTA c (qt = 0..95): amax of the CTA's block range of K and V -> publish (epoch-tagged)
+// -> every CTA's partial -> g = RN32(amax / 2688) -> quantize the range into the slot -> done tag.
+// Cooperative launch: all G CTAs are co-resident, so the partial exchange cannot deadlock.
+// not inlined: its register allocation stays out of the MMA issuer's (same warpgroup, same budget)
+template <int D, int DT>
+__device__ __noinline__ void fused_append_role(const AttnParams& p, uint8_t* smem_ap, int qt, unsigned long long E) {
+#define KVQ_TRACE_AP(ev)                                                           \
+  do {                                                                             \
+    if (p.trace != nullptr && blockIdx.x == 0 && qt == 0) p.trace[63 * 16 + (ev)] = clock64(); \
+  } while (0)
+  KVQ_TRACE_AP(0);
+  constexpr int kNB = D / 16, kUB = 16 * (DT == DT_BF16 ? 2 : 4);
+  const int G = gridDim.x, c = blockIdx.x, H = p.H;
+  const int64_t n = (int64_t)p.Tq * H * D, nblk = n / 16;
+  const int64_t u0 = nblk * c / G, u1 = nblk * (c + 1) / G;
+  unsigned long long* sync = p.ap_sync;
+  uint32_t* red = reinterpret_cast<uint32_t*>(smem_ap + 16);  // [2 tensors][3 warps]
+  float* gsh = reinterpret_cast<float*>(smem_ap + 48);         // g of K, V (NaN bits: non-finite)
+  // ---- A: block maxima (as fp32 bit patterns) over [u0, u1) of K and V, non-finite reported
+  uint32_t m[2] = {0u, 0u};
+#ifdef KVQ_AP_EXPERIMENT_NOWORK  // timing experiment only (wrong bytes): the exchange without the work
+  for (int t = 0; t < 0; ++t) {
+#else
+  for (int t = 0; t < 2; ++t) {
+#endif
+    const uint8_t* x = static_cast<const uint8_t*>(p.ap_x[t]);
+    for (int64_t u = u0 + qt; u < u1; u += 96) {
+      uint32_t bm = 0;
+#pragma unroll
+      for (int k = 0; k < kUB / 16; ++k) bm = max(bm, vec_absmax_bits<DT>(ld_nc_v4(x + u * kUB + 16 * k)));
+      if (bm >= 0x7F800000u)
+        report_status(p.status, -6 /* KVQ_ENONFINITE */,
+                      (unsigned long long)(t * n + u * 16 + first_nonfinite16<DT>(x + u * kUB)));
+      m[t] = max(m[t], bm);
+    }
+  }
+  KVQ_TRACE_AP(1);
+  const int w = qt >> 5;
+  for (int t = 0; t < 2; ++t) {
+    const uint32_t v = warp_max_u32(m[t]);
+    if ((qt & 31) == 0) red[t * 3 + w] = v;
+  }
+  named_bar_sync(6, 96);
+  if (qt == 0)
+    for (int t = 0; t < 2; ++t)
+      st_release_u64(sync + 1 + t * kMaxCtas + c, ((E + 1) << 32) | max(max(red[t * 3], red[t * 3 + 1]), red[t * 3 + 2]));
+  // ---- B: every CTA's partial of this launch (polled in parallel, relaxed) -> the tensor amax -> g
+  uint32_t pa[2] = {0u, 0u};
+  for (int t = 0; t < 2; ++t)
+    for (int i = qt; i < G; i += 96) {
+      unsigned long long v;
+      while (((v = ld_relaxed_u64(sync + 1 + t * kMaxCtas + i)) >> 32) != E + 1) __nanosleep(64);
+      pa[t] = max(pa[t], (uint32_t)v);
+    }
+  named_bar_sync(6, 96);  // every CTA's partial is in (red[] is free again)
+  for (int t = 0; t < 2; ++t) {
+    const uint32_t v = warp_max_u32(pa[t]);
+    if ((qt & 31) == 0) red[t * 3 + w] = v;
+  }
+  named_bar_sync(6, 96);
+  if (qt < 2) {
+    const uint32_t a = max(max(red[qt * 3], red[qt * 3 + 1]), red[qt * 3 + 2]);
+    gsh[qt] = a >= 0x7F800000u ? __uint_as_float(0x7FC00000u) : (a == 0 ? 1.0f : __fdiv_rn(__uint_as_float(a), 2688.0f));
+  }
+  named_bar_sync(6, 96);
+  KVQ_TRACE_AP(2);
+  // ---- C: quantize [u0, u1) into the slot rows (head-major: row h * head_stride_rows + t)
+#ifdef KVQ_AP_EXPERIMENT_NOWORK
+  for (int t = 0; t < 0; ++t) {
+#else
+  for (int t = 0; t < 2; ++t) {
+#endif
+    const float g = gsh[t];
+    if (g != g) continue;  // non-finite tensor: reported, slot bytes undefined (as kv_quantize_append)
+    const float rg = __frcp_rn(g);
+    const bool exact = !(g >= 0x1p-60f && g <= 0x1p60f);
+    const uint8_t* x = static_cast<const uint8_t*>(p.ap_x[t]);
+    for (int64_t u = u0 + qt; u < u1; u += 96) {
+      float v[1][16];
+      unpack_block16<DT>(x + u * kUB, v[0]);
+      uint32_t sb[1], w0[1], w1[1];
+      const uint32_t flags = exact ? 1u : quantize_blocks_fast<1, false>(v, g, rg, sb, w0, w1);
+      if (flags) quantize_block16_exact<false>(v[0], g, sb[0], w0[0], w1[0]);
+      const int64_t row = u / kNB;
+      const int j = (int)(u - row * kNB);
+      const int64_t tt = row / H, h = row - tt * H;
+      const int64_t orow = h * p.head_stride_rows + tt;
+      *reinterpret_cast<uint2*>(p.ap_codes[t] + orow * (D / 2) + j * 8) = make_uint2(w0[0], w1[0]);
+      p.ap_scales[t][orow * kNB + j] = (uint8_t)sb[0];
+    }
+    if (c == 0 && qt == 0) p.ap_g[t] = g;
+  }
+  // ---- D: this CTA's bytes are visible device-wide -> done tag; CTA 0 advances the launch epoch
+  KVQ_TRACE_AP(3);
+  __threadfence();
+  named_bar_sync(6, 96);
+  if (qt == 0) st_release_u64(sync + 1 + 2 * kMaxCtas + c, E + 1);
+  if (c == 0) {  // every CTA has read E (at its start) and finished: advance the launch epoch
+    ap_wait_all_done(sync, G, E, qt, 96);
+    named_bar_sync(6, 96);
+    KVQ_TRACE_AP(4);
+    if (qt == 0) st_release_u64(sync, E + 1);
+  }
+#undef KVQ_TRACE_AP
+}
+
 // SMOOTH (K-smoothing, reading Z20): the cache holds K_bar = K - m per key row,
 // and the score is restored exactly as q.k = q.k_bar + m_j sum_u q_u -- a rank-1 term added in
 // fp32 to the scaled MMA scores before the row max, from the fp32 row sum of the (rounded) Q row
 // and the key means of the tile (one coalesced load per softmax thread, shared through smem).
-template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH, bool QSPLIT>
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH, bool QSPLIT, bool APPEND = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_constant__ AttnParams p) {
   using SM = WsSmem<D, QSPLIT>;
   extern __shared__ uint8_t smem_raw[];
@@ -460,15 +620,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_init(ofree + b, 1);
     }
     fence_mbar_init();
+    if (APPEND) {
+      *reinterpret_cast<unsigned long long*>(smem + SM::kAp) = ld_acquire_u64(p.ap_sync);
+      if (p.trace != nullptr) {  // debug: per-CTA start time (ns)
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        p.trace[1024 + 2 * kMaxCtas + blockIdx.x] = t0;
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // fused append: this launch's epoch, read by thread 0 before any CTA can finish (fused_append_role);
+  // each role re-reads it from shared memory where it needs it, so it does not occupy registers
+  auto launch_epoch = [&]() { return *reinterpret_cast<const volatile unsigned long long*>(smem + SM::kAp); };
+  // Pieces of this CTA and their processing order.  APPEND: a first piece that starts inside a unit is
+  // that unit's tail -- it ends with the unit's last key tiles, the current chunk's -- so it is
+  // processed last, long after the append has finished; every role walks the same order.
+  int npc = 0;
+  bool defer = false;
+  if (APPEND) {
+    Piece t;
+    while (get_piece(sch, c, npc, t)) ++npc;
+    if (npc > 1) {
+      get_piece(sch, c, 0, t);
+      defer = t.tb > 0;
+    }
+  }
+  auto next_piece = [&](int kk, Piece& pc) -> bool {
+    if (!APPEND) return get_piece(sch, c, kk, pc);
+    if (kk >= npc) return false;
+    get_piece(sch, c, defer ? (kk + 1) % npc : kk, pc);
+    return true;
+  };
 
   if (warp < 8) {
     // ================================================================ softmax WG (tile qi)
-    reg_alloc<kRegSoftmax>();
+    reg_alloc<APPEND ? kRegSoftmaxAp : kRegSoftmax>();
     const int qi = warp >> 2;
     const int row = tid & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -477,8 +667,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     int g = 0;  // global tile counter (barrier parity)
     // exponent scale (log2 units); NVFP4-exchanged Q carries g_Q (device scalar) into it
     const float sl2 = p.q_scale ? p.scale_log2 * __ldg(p.q_scale) : p.scale_log2;
+    bool gcur_ok = false;  // APPEND: the appended slot's g, loaded once it is in place
+    float gk_cur = 1.0f, gv_cur = 1.0f;
     Piece pc;
-    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
+    for (int k = 0; next_piece(k, pc); ++k) {
       const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
       const int t = q0 + 128 * qi + row;
       const QRow qr = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(qi), SQL(qi), row, p.Q, p.q_dtype,
@@ -496,8 +688,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, 128);
         float gk = 1.0f, gv = 1.0f;
         if (NVFP4) {
-          gk = __ldg(p.g + 2 * sg.slot);
-          gv = __ldg(p.g + 2 * sg.slot + 1);
+          if (APPEND && sg.slot == p.ap_slot) {  // g of the slot appended by this launch: after CTA 0's done tag
+            if (!gcur_ok) {
+              const unsigned long long Ec = *reinterpret_cast<const volatile unsigned long long*>(smem + SM::kAp);
+              while (ld_relaxed_u64(p.ap_sync + 1 + 2 * kMaxCtas) != Ec + 1) __nanosleep(64);
+              asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              gk_cur = ld_relaxed_f32(p.ap_g);
+              gv_cur = ld_relaxed_f32(p.ap_g + 1);
+              gcur_ok = true;
+            }
+            gk = gk_cur;
+            gv = gv_cur;
+          } else {
+            gk = __ldg(p.g + 2 * sg.slot);
+            gv = __ldg(p.g + 2 * sg.slot + 1);
+          }
         }
         const float cs = gk * sl2q;
         float mean_r = 0.0f;  // SMOOTH: this thread's key of the tile
@@ -729,11 +934,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     }
   } else if (warp < 12) {
     // ================================================================ dequant WG
-    reg_dealloc<kRegDequant>();
+    reg_dealloc<APPEND ? kRegDequantAp : kRegDequant>();
     const int r = tid - 256;  // key row within the tile
     int g = 0;
+    bool ap_ready = false;  // APPEND: every CTA's share of the appended slot is in place
     Piece pc;
-    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
+    for (int k = 0; next_piece(k, pc); ++k) {
       const int h = pc.unit / p.qpairs;
       TileIter it;
       tile_seek(p, pc.tb, it);
@@ -752,8 +958,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         if (NVFP4) {
           const int64_t crow = (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + r;
           PackedRow<D> pk, pv;
-          load_packed_row<D>(pk, p.codes_k + crow * (D / 2), p.scales_k + crow * (D / 16));
-          load_packed_row<D>(pv, p.codes_v + crow * (D / 2), p.scales_v + crow * (D / 16));
+          if (APPEND && sg.slot == p.ap_slot) {  // the chunk being appended by this launch
+            if (!ap_ready) {
+              unsigned long long t0 = 0, t1;
+              if (r == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+              ap_wait_all_done(p.ap_sync, G, launch_epoch(), r, 128);
+              named_bar_sync(5, 128);
+              if (r == 0 && p.trace != nullptr) {  // debug: per-CTA (start of the wait, its length) in ns
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                p.trace[1024 + 2 * c] = t0;
+                p.trace[1024 + 2 * c + 1] = t1 - t0;
+              }
+              ap_ready = true;
+            }
+            load_packed_row<D, true>(pk, p.codes_k + crow * (D / 2), p.scales_k + crow * (D / 16));
+            load_packed_row<D, true>(pv, p.codes_v + crow * (D / 2), p.scales_v + crow * (D / 16));
+          } else {
+            load_packed_row<D>(pk, p.codes_k + crow * (D / 2), p.scales_k + crow * (D / 16));
+            load_packed_row<D>(pv, p.codes_v + crow * (D / 2), p.scales_v + crow * (D / 16));
+          }
           if (g >= SM::kNBuf) mbar_wait(kempty + b, par);
           store_dequant_row<D>(SK(b), r, pk);
           fence_proxy_async_smem();
@@ -783,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       }
     }
   } else {
-    reg_dealloc<kRegMma>();
+    reg_dealloc<APPEND ? kRegMmaAp : kRegMma>();
   }
   if (warp == 12) {
     // ================================================================ MMA issuer warp
@@ -866,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
     };
     int g = 0;
     Piece pc;
-    for (int k = 0; get_piece(sch, c, k, pc); ++k) {
+    for (int k = 0; next_piece(k, pc); ++k) {
       const int np = pc.te - pc.tb;
       mbar_wait(qfull + 0, k & 1);
       mbar_wait(qfull + 1, k & 1);
@@ -963,6 +1186,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       }
       g += np;
     }
+  }
+  if (APPEND && warp >= 13) {  // the MMA warpgroup's three spare warps quantize this CTA's share
+    const unsigned long long E = launch_epoch();
+    if (p.ap_dtype == DT_BF16) fused_append_role<D, DT_BF16>(p, smem + SM::kAp, tid - 13 * 32, E);
+    else fused_append_role<D, DT_FP32>(p, smem + SM::kAp, tid - 13 * 32, E);
   }
   tc_fence_before();
   __syncthreads();
@@ -1399,9 +1627,9 @@ __global__ void __launch_bounds__(512) combine_kernel(const __grid_constant__ At
   }
 }
 
-template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH = false, bool QSPLIT = false>
+template <int D, bool NVFP4, bool MMA_BF16, bool SMOOTH = false, bool QSPLIT = false, bool APPEND = false>
 cudaError_t launch_t(AttnParams p, cudaStream_t st) {
-  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16, SMOOTH, QSPLIT>;
+  auto kern = attn_ws_kernel<D, NVFP4, MMA_BF16, SMOOTH, QSPLIT, APPEND>;
   const int smem = WsSmem<D, QSPLIT>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1427,8 +1655,23 @@ cudaError_t launch_t(AttnParams p, cudaStream_t st) {
   }
   p.grid = G;
   p.ws_slot_floats = 256 * D + 512;
-  kern<<<G, kThreads, smem, st>>>(p);
-  e = cudaGetLastError();
+  if (APPEND) {  // every CTA exchanges its shard amax with all others: co-residency guaranteed or no launch
+    if (p.ws == nullptr || G > kMaxCtas) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+  } else {
+    kern<<<G, kThreads, smem, st>>>(p);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess || !split) return e;
   if (G > 1) combine_kernel<D><<<dim3(G - 1, kCombineSplit), 512, 0, st>>>(p, n);  // per range boundary
   return cudaGetLastError();
@@ -1499,6 +1742,11 @@ cudaError_t preload_attention_kernels() {
   touch_attention<128>(&a);
   touch_attention<64>(&a);
   return cudaGetLastError();
+}
+
+// chunk attention with the chunk's quantize/append fused into the launch (plain NVFP4 mode, bf16 Q)
+cudaError_t launch_attention_append(const AttnParams& p, cudaStream_t st) {
+  return p.d == 128 ? launch_t<128, true, false, false, false, true>(p, st) : launch_t<64, true, false, false, false, true>(p, st);
 }
 
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st) {

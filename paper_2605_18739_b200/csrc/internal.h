@@ -109,6 +109,18 @@ struct AttnParams {
   // pointer, layout [o_Ts, o_H, d]) at row (t - r o_Ts, o_h0 + h); o_peer[0] null = O as usual
   uint8_t* o_peer[kMaxP];
   int o_Ts, o_H, o_h0;
+  // Append fused into the attention launch (chunk_attention_append): the three spare warps of every
+  // CTA's MMA warpgroup quantize CTA c's share of the chunk's K and V into slot ap_slot (definition
+  // R1, quant_core.cuh) while the other warps attend over the history; tiles of ap_slot are read
+  // only once every CTA has finished.  ap_sync: [0] launch epoch E, [1 .. 1+kMaxCtas) shard amax
+  // of K, [.. +kMaxCtas) of V ((E + 1) << 32 | bits), [.. +kMaxCtas) done tags (= E + 1); tags are
+  // E + 1, never 0, so the zeroed arena of a new cache holds no ready-looking word.
+  const void* ap_x[2];       // K, V [T_c, H, d] (ap_dtype), or null: no fused append
+  int ap_dtype, ap_slot;
+  uint8_t* ap_codes[2];      // slot base (head 0) of the codes / scales of K, V
+  uint8_t* ap_scales[2];
+  float* ap_g;               // [2] g of the slot
+  unsigned long long* ap_sync;
   // bf16 KV mode: TMA tensor maps of K and V viewed as [n_keys][H][d] bf16, box {64, 1, 128},
   // 128-byte swizzle (one 128-key x 64-column panel of the K-major SW128 tile per copy)
   CUtensorMap tmap_k, tmap_v;
@@ -117,6 +129,7 @@ struct AttnParams {
 };
 
 constexpr int kMaxCtas = 148;  // workspace sized for one CTA per SM on B200
+constexpr int kApSyncWords = 1 + 3 * kMaxCtas;  // AttnParams::ap_sync
 inline size_t attn_ws_bytes(int d) { return (size_t)2 * kMaxCtas * (256 * d + 512) * sizeof(float); }
 
 // tsr_begin = 1: V only (K's partials then come from launch_smooth_amax)
@@ -131,6 +144,7 @@ cudaError_t launch_quantize_fused(const QuantParams& p, unsigned long long* coun
 cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t st);
 cudaError_t launch_export(const ExportParams& p, cudaStream_t st);
 cudaError_t launch_attention(const AttnParams& p, bool nvfp4_kv, cudaStream_t st);
+cudaError_t launch_attention_append(const AttnParams& p, cudaStream_t st);
 cudaError_t launch_dequant_window(const DequantParams& base, const AttnSeg* segs, int nseg, void* Kout,
                                   void* Vout, cudaStream_t st);
 

@@ -80,6 +80,9 @@ _SIGS = {
     "chunk_attention_bf16kv": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                               ctypes.c_int32, ctypes.c_float, _P, ctypes.c_int, _P]),
     "kvq_bf16kv_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32]),
+    "chunk_attention_append": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, ctypes.c_int, _P, ctypes.c_int,
+                                              ctypes.POINTER(_Mask), ctypes.c_float, _P, ctypes.c_int, _P,
+                                              ctypes.c_size_t, _P]),
     "chunk_attention_bf16kv_ws": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                                  ctypes.c_int32, ctypes.c_float, _P, ctypes.c_int, _P,
                                                  ctypes.c_size_t, _P]),
@@ -264,6 +267,25 @@ class KVCache:
             _check(lib().chunk_attention_ws(self._h, layer, _ptr(Q), _dt(Q), ctypes.byref(m), softmax_scale,
                                             _ptr(out), _out_code(out.dtype), _ptr(workspace), workspace.numel(),
                                             _stream()), "chunk_attention_ws")
+        return out
+
+    def append_attention(self, layer, chunk_index, K, V, Q, mask: Mask, out_dtype=torch.bfloat16, softmax_scale=0.0,
+                         out=None, workspace=None):
+        """chunk_attention_append: append chunk `chunk_index`'s K, V and attend its queries in one launch
+        (the quantization fused into the attention kernel; falls back to the two calls where not fused)."""
+        self._shape_ok(K)
+        self._shape_ok(V)
+        self._shape_ok(Q)
+        if K.dtype != V.dtype:
+            raise KVQError(-3, "K and V dtypes differ")
+        if out is None:
+            out = torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
+        m = mask._c()
+        _check(lib().chunk_attention_append(self._h, layer, chunk_index, _ptr(K), _ptr(V), _dt(K), _ptr(Q), _dt(Q),
+                                            ctypes.byref(m), softmax_scale, _ptr(out), _out_code(out.dtype),
+                                            _ptr(workspace) if workspace is not None else None,
+                                            workspace.numel() if workspace is not None else 0, _stream()),
+               "chunk_attention_append")
         return out
 
     def new_attention_workspace(self):

@@ -2,7 +2,8 @@
     compute-sanitizer --tool memcheck python tools/sanitize_all.py
 Single-pass and two-pass quantize/append (plain, 4/6 search, K-smoothing), dequantize, export,
 window dequant, fused attention (bf16 Q, fp32 Q split, smoothing, bf16 output), bf16-KV attention,
-Ulysses bf16 / NVFP4 (+ NVFP4 Q) / peer exchanges with simulated ranks.  Prints OK at the end."""
+Ulysses bf16 / NVFP4 (+ NVFP4 Q) / peer exchanges with simulated ranks, the persistent TMA bf16-KV
+grid, out-of-fp16-range queries and the f4 direct path (one rank).  Prints OK at the end."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -36,6 +37,20 @@ for d in (64, 128):
             c.dequantize_window(0, kvq.Mask(2, 1, 6))
 q, k, v = synth.make_qkv(150, 3, 128, "bf16", 0, 0)
 kvq.chunk_attention_bf16kv(q.torch(dev), k.torch(dev), v.torch(dev))
+for dd in (64, 128):  # A12 on the persistent grid: TMA-landed tiles, ragged key tail, stream-K partials
+    qb, kb, vb = synth.make_qkv(300, 3, dd, "bf16", 0, 1)
+    kvq.chunk_attention_bf16kv(qb.torch(dev), kb.torch(dev)[:233].contiguous(), vb.torch(dev)[:233].contiguous(),
+                               workspace=kvq.new_bf16kv_workspace(dd, dev))
+# queries outside fp16's range (per-row power-of-two scaling) and a score-range report (reading Z25)
+cz = kvq.KVCache(1, 3, 128, 50, 3, sink_frames=1, window_frames=6, max_chunk_slots=4, device=dev)
+qz, kz, vz = synth.make_qkv(150, 3, 128, "bf16", 0, 0)
+cz.append(0, 0, kz.torch(dev), vz.torch(dev))
+Qz = qz.torch(dev).clone()
+Qz[3] *= 2.0 ** 40
+Qz[7] *= 2.0 ** -40
+cz.attention(0, Qz, kvq.Mask(0, 1, 6), torch.float32)
+cz.attention(0, Qz, kvq.Mask(0, 1, 6), torch.bfloat16, workspace=cz.new_attention_workspace())
+cz.status()
 # exchanges, P = 2 simulated ranks
 P, H, d, T = 2, 5, 128, 120
 Ts = T // P
@@ -76,5 +91,18 @@ for p in range(P):
     pes[p].signal_o(1)
 for r in range(P):
     pes[r].pull_o(1, torch.empty((Ts, H, d), dtype=torch.bfloat16, device=dev))
+# f4 direct (owners' cache slots and O shards written in place), one rank: the sanitizer serializes
+# kernels, so cross-rank device waits would never be satisfied with P > 1 under it
+T1, H1 = 120, 5
+c1 = kvq.KVCache(1, H1, 128, 40, 3, sink_frames=3, window_frames=9, max_chunk_slots=4, device=dev)
+w1 = torch.zeros(kvq.peer_window_bytes(T1, H1, 128, 1), dtype=torch.uint8, device=dev)
+pe1 = kvq.PeerExchange(T1, H1, 128, 1, 0, [w1.data_ptr()])
+pe1.bind_caches(c1, [c1.arena.data_ptr()])
+for ch in range(2):
+    q1, k1, v1 = (x.torch(dev) for x in synth.make_qkv(T1, H1, 128, "bf16", 0, ch))
+    pe1.publish_amax(k1, v1, ch + 1)
+    pe1.append_direct(0, ch, q1, k1, v1, ch + 1)
+    pe1.attention_direct(0, kvq.Mask(ch, 3, 9), ch + 1)
+    pe1.wait_o(ch + 1)
 torch.cuda.synchronize()
 print("OK")
