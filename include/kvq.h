@@ -163,10 +163,12 @@ kvq_status chunk_attention_ws(kvq_cache* cache, int32_t layer, const void* Q, kv
  * warps attend over the history; each CTA reads the new slot only after every CTA has finished
  * (the tensor amax is exchanged between the co-resident CTAs of a cooperative launch), and a
  * first work piece that would reach the new chunk's tiles early is processed last.  The append's
- * own time is hidden behind the history tiles (PAPER.md:146's "<2%" overhead, made ~0).
- * mask->chunk_index must equal chunk_index.  Used when the cache is in the plain mode
- * (scale_mode 0, no K-smoothing), Q is bf16 and the appended chunk is at most half of K_eff;
- * otherwise the call runs kv_quantize_append then chunk_attention(_ws) on the stream.  Errors as
+ * own time would hide behind the history tiles.  MEASURED SLOWER than the two launches on the
+ * Wan layer (the combined kernel's register budget costs more than the 14 us append it hides,
+ * DESIGN.md §5.1), so it is opt-in: environment KVQ_FUSED_APPEND=1, and only in the plain mode
+ * (scale_mode 0, no K-smoothing) with bf16 Q when the appended chunk is at most half of K_eff.
+ * Otherwise the call runs kv_quantize_append then chunk_attention(_ws) on the stream.
+ * mask->chunk_index must equal chunk_index.  Errors as
  * for those two calls (checked before anything is launched).  dev_workspace: NULL = the cache's
  * own, else as chunk_attention_ws. */
 kvq_status chunk_attention_append(kvq_cache* cache, int32_t layer, int64_t chunk_index,

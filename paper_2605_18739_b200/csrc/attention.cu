@@ -467,9 +467,8 @@ KVQ_DEV int first_nonfinite16(const uint8_t* src) {
 // Warps 13-15 of CTA c (qt = 0..95): amax of the CTA's block range of K and V -> publish (epoch-tagged)
 // -> every CTA's partial -> g = RN32(amax / 2688) -> quantize the range into the slot -> done tag.
 // Cooperative launch: all G CTAs are co-resident, so the partial exchange cannot deadlock.
-// not inlined: its register allocation stays out of the MMA issuer's (same warpgroup, same budget)
 template <int D, int DT>
-__device__ __noinline__ void fused_append_role(const AttnParams& p, uint8_t* smem_ap, int qt, unsigned long long E) {
+KVQ_DEV void fused_append_role(const AttnParams& p, uint8_t* smem_ap, int qt, unsigned long long E) {
 #define KVQ_TRACE_AP(ev)                                                           \
   do {                                                                             \
     if (p.trace != nullptr && blockIdx.x == 0 && qt == 0) p.trace[63 * 16 + (ev)] = clock64(); \

@@ -22,6 +22,12 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
+@pytest.fixture(autouse=True)
+def _fused_on(monkeypatch):
+    # the fused launch is opt-in (kvq.h): every test here runs it
+    monkeypatch.setenv("KVQ_FUSED_APPEND", "1")
+
+
 def _need_gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -124,3 +130,20 @@ def test_fused_append_reports_nonfinite():
     c.append_attention(0, 3, K, v.torch(DEV), q.torch(DEV), kvq.Mask(3, 3, 12))
     code, idx = c.status()
     assert code == -6 and idx == (100 * H + 2) * d + 17        # KVQ_ENONFINITE, flat index into K
+
+
+def test_append_attention_default_two_launches(monkeypatch):
+    # without the opt-in the call runs kv_quantize_append + chunk_attention: same bytes, same bar
+    _need_gpu()
+    monkeypatch.delenv("KVQ_FUSED_APPEND", raising=False)
+    H, d, tpf, fc = 4, 128, 256, 3
+    T = tpf * fc
+    c = kvq.KVCache(1, H, d, tpf, fc, sink_frames=3, window_frames=12, max_chunk_slots=6, device=DEV)
+    o = OracleKVCache(1, H, d, tpf, fc)
+    for ch in range(4):
+        q, k, v = synth.make_qkv(T, H, d, "bf16", 4, ch)
+        m = kvq.Mask(ch, 3, 12)
+        O = c.append_attention(0, ch, k.torch(DEV), v.torch(DEV), q.torch(DEV), m, torch.float32).cpu().numpy()
+        o.append(0, ch, k.f64, v.f64)
+        assert_chunk_bytes_equal(c.export(0, ch), nvfp4.quantize_kv_chunk(k.f64), nvfp4.quantize_kv_chunk(v.f64))
+        check_fp32_out(O, o.attend(0, ch, q.f64, 3, 12))

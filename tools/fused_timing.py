@@ -1,6 +1,7 @@
 """Wan layer step (chunk 6, 32,760 keys) as append + attention (two launches) vs the fused
 chunk_attention_append (one launch): CUDA events, L2 flushed before each step, median of 20."""
 import os, sys
+os.environ["KVQ_FUSED_APPEND"] = "1"  # the fused launch is opt-in (kvq.h)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2605_18739_b200 import kvq, synth

@@ -2,6 +2,7 @@
 events (as tools/trace_attn.py), the fused-append phases of CTA 0 (clock64), and for every CTA when it
 first needed the appended slot and how long it waited for it (globaltimer, ns)."""
 import sys, os, ctypes
+os.environ["KVQ_FUSED_APPEND"] = "1"  # the fused launch is opt-in (kvq.h)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
