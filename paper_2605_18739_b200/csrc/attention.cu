@@ -57,9 +57,10 @@ constexpr int kRegSoftmax = KVQ_REG_SOFTMAX, kRegMma = KVQ_REG_MMA, kRegDequant 
 constexpr int kRegSoftmaxAp = KVQ_REG_SOFTMAX_AP, kRegMmaAp = KVQ_REG_MMA_AP,
               kRegDequantAp = 512 - 2 * KVQ_REG_SOFTMAX_AP - KVQ_REG_MMA_AP;
 // Of every 8 exponential pairs of a score row, this many are evaluated by exp2_poly_pair on the
-// FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).
+// FMA pipe instead of MUFU.EX2 (MUFU alone would equal the tensor-core time at d = 128).  Round 2
+// same-box sweeps: 1 -> 886-892 us, 2 -> 910-916 us, 3 -> 937 us (round 1 had found 2 best).
 #ifndef KVQ_POLY_PAIRS
-#define KVQ_POLY_PAIRS 2
+#define KVQ_POLY_PAIRS 1
 #endif
 constexpr int kPolyPairs = KVQ_POLY_PAIRS;
 // Lazy-rescale threshold in log2 units (0 = exact running max, O rescaled whenever it grows).
@@ -83,6 +84,22 @@ constexpr float kLazyLog2 = KVQ_LAZY_LOG2;
 #define KVQ_SP_ROTATE 0
 #endif
 constexpr bool kRotate = KVQ_SP_ROTATE != 0;
+// Split rows (build knob): the two softmax warpgroups work TOGETHER on each query tile -- warpgroup h
+// takes key columns [64 h, 64 h + 64) of every row of S -- and go through the two tiles in turn
+// (tile 0, tile 1, tile 0, ...), instead of one warpgroup per tile.  Each tile's softmax then takes
+// half the time, so the per-tile chain softmax -> PV -> QK -> softmax (P reuses S's TMEM columns)
+// shrinks, while the tensor core still alternates between the tiles.  The halves exchange their
+// partial row maxima through shared memory (one 256-thread named barrier per tile) so both take the
+// same lazy max; the row sums are combined once per piece.  Correct (parity suite) and a tile's
+// softmax does take less time (1,660-1,790 vs 2,180 cycles), but both warpgroups now run their
+// exponential loops at the same time on every SM sub-partition, so MUFU and the FMA pipe are shared
+// and the two tiles' softmax together still take ~3,500 cycles: 898-903 us against 886-892 us for
+// the per-tile design with one polynomial pair in eight.  Off by default.
+#ifndef KVQ_SPLIT_ROWS
+#define KVQ_SPLIT_ROWS 0
+#endif
+constexpr bool kSplitRows = KVQ_SPLIT_ROWS != 0;
+static_assert(!(kSplitRows && kRotate), "split rows and rotating S/P regions are exclusive");
 KVQ_DEV void sp_regions(int k, uint32_t& a, uint32_t& b) {
   if (k < 2) {
     a = 2u * k;
@@ -133,7 +150,10 @@ struct WsSmem {
   // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull[2] ofull[2] + tmem slot
   static constexpr int kMean = kBar + 20 * 8 + 16;  // K-smoothing: [WG][2 buffers][128] fp32 means
   static constexpr int kAp = kMean + 2 * 2 * 128 * 4;  // fused append: launch epoch, shard amax partials
-  static constexpr int kBytes = kAp + 64 + 1024;
+  // split rows: partial row maxima [2 steps][2 halves][128] fp32, query-row info [2 tiles][128] x
+  // (sum(q) * scale, exponent scale, non-finite flag), row sums [2 tiles][2 halves][128]
+  static constexpr int kXch = kAp + 64;
+  static constexpr int kBytes = kXch + 2 * 2 * 128 * 4 + 2 * 128 * 12 + 2 * 2 * 128 * 4 + 1024;
   // K^/V^ buffer of global tile g, and the mbarrier parities of its full / empty waits
   static KVQ_DEV int buf(int g) { return kNBuf == 2 ? (g & 1) : 0; }
   static KVQ_DEV uint32_t full_par(int g) { return kNBuf == 2 ? ((g >> 1) & 1) : (g & 1); }
@@ -612,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
       mbar_init(kempty + b, 1);
       mbar_init(vempty + b, 1);
       mbar_init(sfull + b, 1);
-      mbar_init(pfull + b, 128);
+      mbar_init(pfull + b, kSplitRows ? 256 : 128);  // split rows: both halves of every row arrive
       mbar_init(ofull + b, 1);
       mbar_init(qfull + b, 128);
       mbar_init(sfree + b, 128);
@@ -656,6 +676,255 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
   };
 
   if (warp < 8) {
+   if constexpr (kSplitRows) {
+    // ================================================================ softmax, split rows (kSplitRows)
+    reg_alloc<APPEND ? kRegSoftmaxAp : kRegSoftmax>();
+    const int half = warp >> 2;  // this warpgroup's key columns of every row: [64 half, 64 half + 64)
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    float* pmax = reinterpret_cast<float*>(smem + SM::kXch);  // [2 step parities][2 halves][128]
+    float* qinf = pmax + 2 * 2 * 128;                          // [2 tiles][128][3]
+    float* lsum = qinf + 2 * 128 * 3;                          // [2 tiles][2 halves][128]
+    int g = 0;     // key-tile counter (barrier parity; both query tiles advance together)
+    int step = 0;  // (key tile, query tile) steps: exchange-buffer parity
+    const float sl2 = p.q_scale ? p.scale_log2 * __ldg(p.q_scale) : p.scale_log2;
+    bool gcur_ok = false;  // APPEND: the appended slot's g, loaded once it is in place
+    float gk_cur = 1.0f, gv_cur = 1.0f;
+    Piece pc;
+    for (int k = 0; next_piece(k, pc); ++k) {
+      const int h = pc.unit / p.qpairs, q0 = (pc.unit - h * p.qpairs) * 256;
+      {  // warpgroup `half` loads query tile `half` and publishes each row's scales for both halves
+        const int tq = q0 + 128 * half + row;
+        const QRow qr = load_q_row<D, MMA_BF16, SMOOTH, QSPLIT>(SQ(half), SQL(half), row, p.Q, p.q_dtype,
+                                                                (int64_t)tq * H + h, tq < p.Tq, p.status);
+        float* q3 = qinf + (half * 128 + row) * 3;
+        q3[0] = qr.qsum * sl2;
+        q3[1] = sl2 * qr.qscale;  // this row's exponent scale (Q was scaled by 1/qscale)
+        q3[2] = qr.nonfinite ? 1.0f : 0.0f;
+        fence_proxy_async_smem();
+        mbar_arrive(qfull + half);
+      }
+      named_bar_sync(8, 256);
+      float sl2q[2], qsb[2], m_run[2], l_run[2], gv_run[2];
+      bool rrep[2];
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi) {
+        const float* q3 = qinf + (qi * 128 + row) * 3;
+        qsb[qi] = q3[0];
+        sl2q[qi] = q3[1];
+        rrep[qi] = q3[2] != 0.0f;
+        m_run[qi] = -INFINITY;
+        l_run[qi] = 0.0f;
+        gv_run[qi] = 1.0f;
+      }
+      TileIter it;
+      tile_seek(p, pc.tb, it);
+      for (int j = 0; j < pc.te - pc.tb; ++j, ++g, tile_next(p, it)) {
+        const AttnSeg& sg = p.seg[it.seg];
+        const int lo = max(sg.begin - it.t0, 0), hi = min(sg.end - it.t0, 128);
+        float gk = 1.0f, gv = 1.0f;
+        if (NVFP4) {
+          if (APPEND && sg.slot == p.ap_slot) {  // g of the slot appended by this launch: after CTA 0's done tag
+            if (!gcur_ok) {
+              const unsigned long long Ec = *reinterpret_cast<const volatile unsigned long long*>(smem + SM::kAp);
+              while (ld_relaxed_u64(p.ap_sync + 1 + 2 * kMaxCtas) != Ec + 1) __nanosleep(64);
+              asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              gk_cur = ld_relaxed_f32(p.ap_g);
+              gv_cur = ld_relaxed_f32(p.ap_g + 1);
+              gcur_ok = true;
+            }
+            gk = gk_cur;
+            gv = gv_cur;
+          } else {
+            gk = __ldg(p.g + 2 * sg.slot);
+            gv = __ldg(p.g + 2 * sg.slot + 1);
+          }
+        }
+        float mean_r = 0.0f;  // SMOOTH: key `row`'s mean, loaded by half 0, shared through smem
+        if (SMOOTH && half == 0 && row >= lo && row < hi)
+          mean_r = __ldg(p.mean_k + (int64_t)h * p.head_stride_rows + (int64_t)sg.slot * p.T_pad + it.t0 + row);
+#pragma unroll  // the per-tile-pair state (m_run[qi], ...) stays in registers
+        for (int qi = 0; qi < 2; ++qi, ++step) {
+          const uint32_t tS = tmem + 128 * qi + lane_off;
+          const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
+          const float cs = gk * sl2q[qi];
+          KVQ_TRACE(g, 3 * qi + 0);
+          mbar_wait(sfull + qi, g & 1);
+          KVQ_TRACE(g, 3 * qi + 1);
+          tc_fence_after();
+          uint32_t s[64];
+          KVQ_TMEM_LD32(tS + 64 * half, s);
+          KVQ_TMEM_LD32(tS + 64 * half + 32, (s + 32));
+          if (SMOOTH && qi == 0 && half == 0)
+            (reinterpret_cast<float*>(smem + SM::kMean) + (j & 1) * 128)[row] = mean_r;
+          tmem_ld_wait();
+          KVQ_TRACE_SM(g, 12);
+          if (SMOOTH) {  // y = s * cs + m_j * sum(q) * scale_log2 (log2 units), in place
+            if (qi == 0) named_bar_sync(8, 256);  // the tile's key means are in place
+            const float* mbuf = reinterpret_cast<const float*>(smem + SM::kMean) + (j & 1) * 128 + 64 * half;
+            const uint64_t cs2s = f32x2_pack(cs, cs), qsb2 = f32x2_pack(qsb[qi], qsb[qi]);
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+              const float2 m2 = reinterpret_cast<const float2*>(mbuf)[kk];
+              const uint64_t b2 = fmul2(f32x2_pack(m2.x, m2.y), qsb2);
+              const uint64_t y2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2s, b2);
+              float y0, y1;
+              f32x2_unpack(y2, y0, y1);
+              s[2 * kk] = __float_as_uint(y0);
+              s[2 * kk + 1] = __float_as_uint(y1);
+            }
+          }
+          // this half's row max over valid keys (column 64 half + kk)
+          const int clo = lo - 64 * half, chi = hi - 64 * half;
+          if (clo > 0 || chi < 64) {
+#pragma unroll
+            for (int kk = 0; kk < 64; ++kk)
+              if (kk < clo || kk >= chi) s[kk] = __float_as_uint(-INFINITY);
+          }
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int kk = 0; kk < 64; kk += 8) {
+            mx0 = fmax3(mx0, __uint_as_float(s[kk]), __uint_as_float(s[kk + 1]));
+            mx1 = fmax3(mx1, __uint_as_float(s[kk + 2]), __uint_as_float(s[kk + 3]));
+            mx2 = fmax3(mx2, __uint_as_float(s[kk + 4]), __uint_as_float(s[kk + 5]));
+            mx3 = fmax3(mx3, __uint_as_float(s[kk + 6]), __uint_as_float(s[kk + 7]));
+          }
+          float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+          // the row's max = max of both halves' (double-buffered by step parity)
+          pmax[((step & 1) * 2 + half) * 128 + row] = mx;
+          named_bar_sync(8, 256);
+          mx = fmaxf(mx, pmax[((step & 1) * 2 + (half ^ 1)) * 128 + row]);
+          // lazy max, identical in both halves (same inputs): see the per-tile design
+          const float m_tile = SMOOTH ? mx : mx * cs;
+          const float m_new = (j == 0 || m_tile > m_run[qi] + kLazyLog2) ? fmaxf(m_run[qi], m_tile) : m_run[qi];
+          const float alpha = ex2_approx(m_run[qi] - m_new);
+          KVQ_TRACE_SM(g, 13);
+          const float cse = SMOOTH ? 1.0f : cs;
+          const uint64_t cs2 = f32x2_pack(cse, cse), mneg2 = f32x2_pack(-m_new, -m_new);
+          uint64_t acc0 = 0, acc1 = 0;
+          float la[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) {
+            const uint64_t x2 = ffma2(f32x2_pack(__uint_as_float(s[2 * kk]), __uint_as_float(s[2 * kk + 1])), cs2, mneg2);
+            float x0, x1, p0, p1;
+            f32x2_unpack(x2, x0, x1);
+            if ((kk & 7) < kPolyPairs) {
+              exp2_poly_pair(x0, x1, p0, p1);
+            } else {
+              p0 = ex2_approx(x0);
+              p1 = ex2_approx(x1);
+            }
+            const uint32_t pk = MMA_BF16 ? pack_bf162(p0, p1) : pack_half2(p0, p1);
+            s[kk] = pk;
+            if (MMA_BF16) {
+              const uint64_t r2 = f32x2_pack(__uint_as_float(pk << 16), __uint_as_float(pk & 0xFFFF0000u));
+              if (kk & 1) acc1 = fadd2(acc1, r2);
+              else acc0 = fadd2(acc0, r2);
+            } else {
+              asm("{ .reg .b16 l, h;\n mov.b32 {l, h}, %4;\n add.rn.f32.f16 %0, l, %0;\n add.rn.f32.f16 %1, h, %1;\n}"
+                  : "+f"(la[(kk & 1) * 2]), "+f"(la[(kk & 1) * 2 + 1]) : "f"(0.0f), "f"(0.0f), "r"(pk));
+            }
+          }
+          float a0, a1, b0, b1;
+          f32x2_unpack(acc0, a0, a1);
+          f32x2_unpack(acc1, b0, b1);
+          l_run[qi] = l_run[qi] * alpha + ((a0 + a1) + (b0 + b1)) + ((la[0] + la[1]) + (la[2] + la[3]));
+          KVQ_TRACE_SM(g, 14);
+          // P of this half's 64 keys = 32 fp16x2 columns at [32 half, +32) of S_qi (the other half has
+          // loaded its S: both passed the barrier above)
+          KVQ_TMEM_ST32(tS + 32 * half, s);
+          if (j > 0) {  // O_qi (this half's D/2 columns) in units of the current chunk's g_V
+            const float f = alpha * (gv_run[qi] / gv);
+            if (!__all_sync(0xffffffffu, f == 1.0f)) {
+              const uint64_t f2 = f32x2_pack(f, f);
+              uint32_t* o = s + 32;  // the upper half of s[] is free once P is packed
+#pragma unroll
+              for (int cc = 0; cc < D / 64; ++cc) {
+                const uint32_t ta = tO + (D / 2) * half + 32 * cc;
+                KVQ_TMEM_LD32(ta, o);
+                tmem_ld_wait();
+#pragma unroll
+                for (int kk = 0; kk < 32; kk += 2) {
+                  float x0, x1;
+                  f32x2_unpack(fmul2(f32x2_pack(__uint_as_float(o[kk]), __uint_as_float(o[kk + 1])), f2), x0, x1);
+                  o[kk] = __float_as_uint(x0);
+                  o[kk + 1] = __float_as_uint(x1);
+                }
+                KVQ_TMEM_ST32(ta, o);
+              }
+            }
+          }
+          gv_run[qi] = gv;
+          m_run[qi] = m_new;
+          tmem_st_wait();
+          KVQ_TRACE_SM(g, 15);
+          tc_fence_before();
+          mbar_arrive(pfull + qi);
+          KVQ_TRACE(g, 3 * qi + 2);
+        }
+      }
+      // ---- piece epilogue: combine the halves' row sums (fixed order: half 0 + half 1)
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi) lsum[(qi * 2 + half) * 128 + row] = l_run[qi];
+      named_bar_sync(8, 256);
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi) {
+        const float l_tot = lsum[(qi * 2) * 128 + row] + lsum[(qi * 2 + 1) * 128 + row];
+        const int t = q0 + 128 * qi + row;
+        const uint32_t tO = tmem + 256 + 128 * qi + lane_off;
+        // score range (reading Z25), as in the per-tile design
+        if (half == 0 && !(fabsf(m_run[qi]) < kScoreRangeLog2) && !rrep[qi] && t < p.Tq)
+          report_status(p.status, -7 /* KVQ_ERANGE */, (unsigned long long)(((int64_t)t * H + h) * D));
+        mbar_wait(ofull + qi, k & 1);
+        tc_fence_after();
+        const float f = pc.full ? gv_run[qi] / l_tot : gv_run[qi];
+        float* wsO = p.ws + (size_t)pc.slot * p.ws_slot_floats + (size_t)(128 * qi + row) * D;
+        if (!pc.full && t < p.Tq && half == 0) {
+          float* wml = p.ws + (size_t)pc.slot * p.ws_slot_floats + 256 * D;
+          wml[128 * qi + row] = m_run[qi];
+          wml[256 + 128 * qi + row] = l_tot;
+        }
+#pragma unroll
+        for (int cc = 0; cc < D / 64; ++cc) {  // this half's D/2 columns, 32 at a time
+          const int col = (D / 2) * half + 32 * cc;
+          uint32_t o[32];
+          KVQ_TMEM_LD32(tO + col, o);
+          tmem_ld_wait();
+          if (t < p.Tq) {
+            if (!pc.full) {
+              float4* dst = reinterpret_cast<float4*>(wsO + col);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                dst[kk] = make_float4(__uint_as_float(o[4 * kk]) * f, __uint_as_float(o[4 * kk + 1]) * f,
+                                      __uint_as_float(o[4 * kk + 2]) * f, __uint_as_float(o[4 * kk + 3]) * f);
+            } else {
+              const int64_t base = ((int64_t)t * H + h) * D + col;
+              if (p.out_dtype == DT_FP32) {
+                float4* dst = reinterpret_cast<float4*>((float*)p.O + base);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  dst[kk] = make_float4(__uint_as_float(o[4 * kk]) * f, __uint_as_float(o[4 * kk + 1]) * f,
+                                        __uint_as_float(o[4 * kk + 2]) * f, __uint_as_float(o[4 * kk + 3]) * f);
+              } else {
+                uint4* dst = reinterpret_cast<uint4*>((__nv_bfloat16*)p.O + base);
+                if (p.o_peer[0] != nullptr) {  // f4 direct: straight into the owning rank's O shard
+                  const int r = t / p.o_Ts;
+                  dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_peer[r]) +
+                                                 ((int64_t)(t - r * p.o_Ts) * p.o_H + p.o_h0 + h) * D + col);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  dst[kk] = make_uint4(pack_bf162(__uint_as_float(o[8 * kk]) * f, __uint_as_float(o[8 * kk + 1]) * f),
+                                       pack_bf162(__uint_as_float(o[8 * kk + 2]) * f, __uint_as_float(o[8 * kk + 3]) * f),
+                                       pack_bf162(__uint_as_float(o[8 * kk + 4]) * f, __uint_as_float(o[8 * kk + 5]) * f),
+                                       pack_bf162(__uint_as_float(o[8 * kk + 6]) * f, __uint_as_float(o[8 * kk + 7]) * f));
+              }
+            }
+          }
+        }
+      }
+    }
+   } else {
     // ================================================================ softmax WG (tile qi)
     reg_alloc<APPEND ? kRegSoftmaxAp : kRegSoftmax>();
     const int qi = warp >> 2;
@@ -931,6 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
         }
       }
     }
+   }
   } else if (warp < 12) {
     // ================================================================ dequant WG
     reg_dealloc<APPEND ? kRegDequantAp : kRegDequant>();
