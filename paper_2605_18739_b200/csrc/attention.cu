@@ -38,10 +38,12 @@ namespace {
 
 constexpr int kThreads = 16 * 32;  // 4 warpgroups: softmax0, softmax1, dequant, MMA (+3 idle warps)
 // Register budget per SM sub-partition (16K regs = 4 warps x 128 at launch), rebalanced with
-// setmaxnreg: softmax 176 + 176, dequant 80, MMA warpgroup 80 (sum 512 per thread slot).  Swept
-// (tools/sweep_attn_flags.sh): 160 / 168 / 176 / 184 -> 858 / 843 / 839 / 923 us graph-timed; 176 kept.
+// setmaxnreg: softmax 168 + 168, dequant 88, MMA warpgroup 88 (sum 512 per thread slot).  Swept
+// (tools/ab_attn.sh, same box, after the debug trace was compiled out -- KVQ_TRACE_BUILD): softmax
+// 160 / 168 / 176 -> 919 (spills) / 832 / 861 us after an L2 flush; at 168 the MMA/dequant split
+// 80/96, 88/88, 96/80 is 830 / 832 / 830 us (noise).  Round 1 (trace compiled in) had found 176.
 #ifndef KVQ_REG_SOFTMAX
-#define KVQ_REG_SOFTMAX 176
+#define KVQ_REG_SOFTMAX 168
 #endif
 #ifndef KVQ_REG_MMA
 #define KVQ_REG_MMA (256 - KVQ_REG_SOFTMAX)
@@ -427,7 +429,12 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
   it.t0 = (p.seg[s].begin & ~127) + 128 * tb;
 }
 
-// debug timeline (CTA 0, first 64 tiles): SM clock at role events, only when p.trace != null
+// debug timeline (CTA 0, first 64 tiles): SM clock at role events, only when p.trace != null, and
+// compiled in only with -DKVQ_TRACE_BUILD=1 (tools/trace_attn.py): the runtime check alone cost the
+// MMA warp (80 registers) two spill/fill pairs per tile in its issue loop.
+#ifndef KVQ_TRACE_BUILD
+#define KVQ_TRACE_BUILD 0
+#endif
 #ifdef KVQ_TRACE_SOFTMAX
 #define KVQ_TRACE_SM(tile, ev) \
   do {                                                                                             \
@@ -438,11 +445,17 @@ KVQ_DEV void tile_seek(const AttnParams& p, int tb, TileIter& it) {
   do {                         \
   } while (0)
 #endif
+#if KVQ_TRACE_BUILD
 #define KVQ_TRACE(tile, ev)                                                                        \
   do {                                                                                           \
     if (p.trace != nullptr && blockIdx.x == 0 && (tile) < 64 && ((tid & 127) == 0 || tid == 384)) \
       p.trace[(tile) * 16 + (ev)] = clock64();                                                   \
   } while (0)
+#else
+#define KVQ_TRACE(tile, ev) \
+  do {                      \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------------------------------------
 // Append fused into the attention launch (AttnParams::ap_*; kv_quantize_append's bytes exactly:

@@ -1,4 +1,5 @@
-"""Print the CTA-0 role timeline of chunk_attention on the Wan layer (development aid)."""
+"""Print the CTA-0 role timeline of chunk_attention on the Wan layer (development aid).
+Needs a build with the trace points compiled in: KVQ_NVCC_FLAGS=-DKVQ_TRACE_BUILD=1 (attention.cu)."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -1,6 +1,7 @@
 """Timeline of the fused append + attention launch on the Wan layer (development aid): CTA 0's role
 events (as tools/trace_attn.py), the fused-append phases of CTA 0 (clock64), and for every CTA when it
-first needed the appended slot and how long it waited for it (globaltimer, ns)."""
+first needed the appended slot and how long it waited for it (globaltimer, ns).
+Needs a build with the trace points compiled in: KVQ_NVCC_FLAGS=-DKVQ_TRACE_BUILD=1 (attention.cu)."""
 import sys, os, ctypes
 os.environ["KVQ_FUSED_APPEND"] = "1"  # the fused launch is opt-in (kvq.h)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
