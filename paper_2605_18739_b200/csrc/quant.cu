@@ -450,6 +450,8 @@ struct RowCursor {
   }
 };
 
+// per-CTA phase timeline (tools/trace_quant.py): compiled in only with -DKVQ_TRACE_BUILD=1
+#if KVQ_TRACE_BUILD
 #define SPTRACE(ev)                                                                      \
   do {                                                                                   \
     if (p.trace != nullptr && tid == 0 && c < 256) {                                     \
@@ -458,6 +460,11 @@ struct RowCursor {
       p.trace[c * 16 + (ev)] = t_;                                                       \
     }                                                                                    \
   } while (0)
+#else
+#define SPTRACE(ev) \
+  do {              \
+  } while (0)
+#endif
 
 template <int DT, int D, int MODE>
 __global__ void __launch_bounds__(kSpThreads, 1)
