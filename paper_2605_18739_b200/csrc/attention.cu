@@ -1130,23 +1130,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
               mbar_wait(ofree + qi, (g - 1) & 1);
               tc_fence_after();
             }
-            // two 32-column chunks per TMEM round trip, staged in the free half of s[]
             const uint64_t f2 = f32x2_pack(f, f);
 #pragma unroll
-            for (int cc = 0; cc < D / 32; cc += 2) {
+            for (int cc = 0; cc < D / 32; ++cc) {  // one 32-column chunk per TMEM round trip
               uint32_t* o = s + 64;
               KVQ_TMEM_LD32(tO + 32 * cc, o);
-              if (D / 32 > 1) KVQ_TMEM_LD32(tO + 32 * (cc + 1), (o + 32));
               tmem_ld_wait();
 #pragma unroll
-              for (int kk = 0; kk < (D / 32 > 1 ? 64 : 32); kk += 2) {
+              for (int kk = 0; kk < 32; kk += 2) {
                 float x0, x1;
                 f32x2_unpack(fmul2(f32x2_pack(__uint_as_float(o[kk]), __uint_as_float(o[kk + 1])), f2), x0, x1);
                 o[kk] = __float_as_uint(x0);
                 o[kk + 1] = __float_as_uint(x1);
               }
               KVQ_TMEM_ST32(tO + 32 * cc, o);
-              if (D / 32 > 1) KVQ_TMEM_ST32(tO + 32 * (cc + 1), (o + 32));
             }
           }
         }
