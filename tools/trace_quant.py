@@ -1,7 +1,8 @@
 """Phase timeline (ns, globaltimer, median/max over CTAs) of the single-pass quantize kernel in steady
 state (development aid).  Events per CTA (thread 0): 0 start, 1 K landed + published, 5 K barrier
 seen (thread 0 is a K poller during A(V)), 6 V landed + published, 8 K table, 10/12 K loop
-iterations 1/2 done, 3 K quantized, 2 V barrier, 9 V table, 11/13 V iterations, 7 V quantized."""
+iterations 1/2 done, 3 K quantized, 2 V barrier, 9 V table, 11/13 V iterations, 7 V quantized.
+Needs a build with the trace points compiled in: KVQ_NVCC_FLAGS=-DKVQ_TRACE_BUILD=1 (quant.cu)."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
