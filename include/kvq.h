@@ -436,7 +436,10 @@ kvq_status kvq_comm_configure(kvq_comm* comm, int32_t num_heads, int32_t exchang
  * Every argument and cache-side error (chunk not appendable, no free slot, a mask chunk not
  * resident after the append's evictions) is returned before the first collective is issued, so
  * a rank that fails never leaves its peers blocked in a collective -- provided every rank passes
- * the same layer, chunk_index and mask. */
+ * the same layer, chunk_index and mask.  Not supported inside CUDA graph capture: a capture and
+ * replay of the world-1 step (NCCL send/recv to self) did not complete on the B200 box; the
+ * single-GPU calls (kv_quantize_append, chunk_attention, chunk_attention_append) are capturable
+ * and replay-tested. */
 kvq_status ulysses_chunk_attention(kvq_comm* comm, kvq_cache* cache, int32_t layer,
                                    int64_t chunk_index, const void* Q_shard, const void* K_shard,
                                    const void* V_shard, kvq_dtype in_dtype, const kvq_mask* mask,
