@@ -1124,7 +1124,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_ws_kernel(const __grid_const
 #else
         if (j > 0) {
 #endif
-          const float f = alpha * (gv_run / gv);
+          // (gv is the tile's slot scale, uniform: the IEEE division only runs on a chunk change)
+          const float f = gv == gv_run ? alpha : alpha * (gv_run / gv);
           if (!__all_sync(0xffffffffu, f == 1.0f)) {
             if (kRotate) {  // this tile's QK no longer orders PV_i(j-1) before us: wait for it
               mbar_wait(ofree + qi, (g - 1) & 1);
